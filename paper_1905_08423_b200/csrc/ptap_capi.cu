@@ -1,0 +1,922 @@
+// ptap_capi.cu -- extern "C" entry points (include/ptap_b200.h) and the
+// device-resident TripleProductPlan.
+//
+// The plan owns every device buffer it allocates (cudaMallocAsync on the
+// caller's stream) and books each under one of the reference's ledger
+// categories (src/ledger.py:23-34):
+//   output_matrix        C (row offsets, columns, values)
+//   auxiliary_matrices   two-step only: C~ = A P, the transposes of P, its staging
+//   transient_hash_peak  arenas, work estimates, count arrays (freed by the end of symbolic)
+//   plan_cache           bin row lists, all-at-once staging, received-slot map, transpose permutations
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ptap_b200.h"
+#include "ptap_kernels.cuh"
+
+using namespace ptapdev;
+
+namespace {
+
+thread_local std::string g_err;
+
+ptap_status fail(ptap_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+enum Cat { CAT_INPUT = 0, CAT_OUTPUT = 1, CAT_AUX = 2, CAT_TRANSIENT = 3, CAT_PLAN = 4 };
+
+#define CK(x)                                                                                            \
+  do {                                                                                                   \
+    cudaError_t _e = (x);                                                                                \
+    if (_e != cudaSuccess)                                                                               \
+      return fail(_e == cudaErrorMemoryAllocation ? PTAP_ERR_OOM : PTAP_ERR_CUDA,                        \
+                  std::string(#x) + ": " + cudaGetErrorString(_e));                                      \
+  } while (0)
+
+#define CKS(x)                                   \
+  do {                                                 \
+    ptap_status _s = (x);                              \
+    if (_s != PTAP_OK) return _s;                      \
+  } while (0)
+
+struct Alloc {
+  size_t bytes;
+  int cat;
+};
+
+struct BinSet {
+  int32_t *rows[NBINS] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t count[NBINS] = {0, 0, 0, 0};
+  int log2t_global = 0;             // table size of the global-memory bin
+  unsigned char *gtables = nullptr; // global tables for the heavy bin
+  int64_t selected = 0;             // rows selected (reference row-kernel calls)
+  bool identity0 = false;           // bin 0 holds every row in order (rows[0] == nullptr)
+};
+
+struct Transpose {
+  int64_t nrows = 0, nnz = 0;
+  int64_t *rp = nullptr;
+  int32_t *row = nullptr;
+  int64_t *perm = nullptr;
+  double *val = nullptr;
+};
+
+}  // namespace
+
+struct ptap_plan {
+  int alg = 0;
+  int64_t nloc = 0, m = 0, c_lo = 0, c_hi = 0, ncl = 0, colmap_len = 0;
+  std::map<void *, Alloc> allocs;
+  int64_t cur[5] = {0, 0, 0, 0, 0}, peak[5] = {0, 0, 0, 0, 0};
+  int64_t prod_cur = 0, prod_peak = 0, total_cur = 0, total_peak = 0;
+  int *d_status = nullptr;
+  unsigned long long *d_u64 = nullptr;  // 16 scratch counters
+  bool released = false;
+  bool symbolic_done = false;
+  BinSet bins_send, bins_local, bins_all, bins_ptd, bins_pto;
+  // transient state carried from symbolic_send to symbolic_local
+  int64_t *ap_nnz = nullptr;
+  Arena local_arena{nullptr, 0};
+  unsigned long long bound_local = 0, bound_send = 0, sum_ap = 0;
+  // C
+  int64_t c_nnz = 0;
+  int64_t *c_rp = nullptr;
+  int32_t *c_col = nullptr;
+  double *c_val = nullptr;
+  // staging
+  int64_t s_nrows = 0, s_nnz = 0;
+  int32_t *s_rows = nullptr;
+  int64_t *s_rp = nullptr;
+  int32_t *s_col = nullptr;
+  double *s_val = nullptr;
+  // received merge map
+  int64_t r_nnz = 0;
+  int64_t *r_slot = nullptr;
+  std::vector<int64_t> r_src_nnz_off;
+  // two-step
+  int64_t ct_nnz = 0;
+  int64_t *ct_rp = nullptr;
+  int32_t *ct_col = nullptr;
+  double *ct_val = nullptr;
+  Transpose ptd, pto;
+  ptap_counters cnt{};
+};
+
+namespace {
+
+ptap_status palloc_raw(ptap_plan *p, void **out, size_t bytes, int cat, cudaStream_t st) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);
+  void *ptr = nullptr;
+  cudaError_t e = cudaMallocAsync(&ptr, bytes, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? PTAP_ERR_OOM : PTAP_ERR_CUDA,
+                std::string("cudaMallocAsync(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  p->allocs[ptr] = Alloc{bytes, cat};
+  p->cur[cat] += bytes;
+  if (p->cur[cat] > p->peak[cat]) p->peak[cat] = p->cur[cat];
+  if (cat != CAT_INPUT) {
+    p->prod_cur += bytes;
+    if (p->prod_cur > p->prod_peak) p->prod_peak = p->prod_cur;
+  }
+  p->total_cur += bytes;
+  if (p->total_cur > p->total_peak) p->total_peak = p->total_cur;
+  *out = ptr;
+  return PTAP_OK;
+}
+
+template <typename T>
+ptap_status palloc(ptap_plan *p, T **out, int64_t count, int cat, cudaStream_t st) {
+  void *v = nullptr;
+  ptap_status s = palloc_raw(p, &v, (size_t)(count > 0 ? count : 1) * sizeof(T), cat, st);
+  *out = (T *)v;
+  return s;
+}
+
+template <typename T>
+void pfree(ptap_plan *p, T *&ptr, cudaStream_t st) {
+  if (!ptr) return;
+  auto it = p->allocs.find((void *)ptr);
+  if (it != p->allocs.end()) {
+    p->cur[it->second.cat] -= it->second.bytes;
+    if (it->second.cat != CAT_INPUT) p->prod_cur -= it->second.bytes;
+    p->total_cur -= it->second.bytes;
+    p->allocs.erase(it);
+  }
+  cudaFreeAsync((void *)ptr, st);
+  ptr = nullptr;
+}
+
+Ops make_ops(const ptap_operands *o) {
+  Ops op;
+  op.nloc = o->n_local; op.m = o->m_global; op.c_lo = o->c_lo; op.c_hi = o->c_hi;
+  op.ad_rp = o->a_diag.row_ptr; op.ad_col = o->a_diag.col; op.ad_val = o->a_diag.val;
+  op.ao_rp = o->a_off.nnz > 0 ? o->a_off.row_ptr : nullptr; op.ao_col = o->a_off.col; op.ao_val = o->a_off.val;
+  op.pd_rp = o->p_diag.row_ptr; op.pd_col = o->p_diag.col; op.pd_val = o->p_diag.val;
+  op.po_rp = o->p_off.nnz > 0 ? o->p_off.row_ptr : nullptr; op.po_col = o->p_off.col; op.po_val = o->p_off.val;
+  op.p_colmap = o->p_colmap;
+  op.pr_rp = o->p_remote.row_ptr; op.pr_col = o->p_remote.col; op.pr_val = o->p_remote.val;
+  return op;
+}
+
+ptap_status validate(const ptap_operands *o) {
+  if (!o) return fail(PTAP_ERR_VALUE, "null operands");
+  if (o->a_diag.nrows != o->n_local || o->p_diag.nrows != o->n_local)
+    return fail(PTAP_ERR_PARTITION, "A and P must share the rank's row block");
+  if (o->a_diag.ncols != o->n_local)
+    return fail(PTAP_ERR_PARTITION, "the column partition of A must equal the row partition of P");
+  if (o->c_lo < 0 || o->c_hi < o->c_lo || o->c_hi > o->m_global || o->p_diag.ncols != o->c_hi - o->c_lo)
+    return fail(PTAP_ERR_PARTITION, "P's diagonal block does not match the owned coarse range");
+  if (o->m_global > 0 && (double)o->m_global * (double)o->m_global >= 4.611686018427388e18)
+    return fail(PTAP_ERR_PARTITION, "output dimension too large for combined row/col keys");
+  if (o->m_global >= (int64_t)INT32_MAX) return fail(PTAP_ERR_VALUE, "coarse dimension exceeds int32 columns");
+  if (o->a_off.nnz > 0 && (o->a_off.nrows != o->n_local || o->a_off.ncols != o->p_remote.nrows))
+    return fail(PTAP_ERR_DRIFT, "gathered rows do not match A's off-diagonal columns");
+  if (o->p_off.nnz > 0 && (o->p_off.nrows != o->n_local || o->p_off.ncols != o->p_colmap_len))
+    return fail(PTAP_ERR_PARTITION, "P's off-diagonal block does not match its column map");
+  return PTAP_OK;
+}
+
+ptap_status read_status(ptap_plan *p, cudaStream_t st, int *out) {
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(out, p->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(p->d_status, 0, sizeof(int)));
+  return PTAP_OK;
+}
+
+ptap_status status_to_error(int s, const char *where) {
+  if (s & ST_ROW_TOO_WIDE) return fail(PTAP_ERR_VALUE, std::string(where) + ": a row exceeds 8192 entries");
+  if (s & ST_DRIFT)
+    return fail(PTAP_ERR_DRIFT, std::string(where) + ": numeric data does not match the symbolic structure");
+  if (s & ST_TABLE_FULL) return fail(PTAP_ERR_DRIFT, std::string(where) + ": a row outgrew its symbolic size");
+  return PTAP_OK;
+}
+
+int ceil_log2(unsigned long long v) {
+  int l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+// ---- bins -------------------------------------------------------------------
+LaunchShape shape_for(int q, const BinSet &bs) {
+  LaunchShape s{};
+  s.gtables = nullptr;
+  s.max_ctas = 148 * 64;
+  switch (q) {
+    case 0: s.group = 8; s.warps = 8; s.log2t = 6; break;
+    case 1: s.group = 32; s.warps = 8; s.log2t = 9; break;
+    case 2: s.group = 32; s.warps = 2; s.log2t = 12; break;
+    default:
+      s.group = 32; s.warps = 4; s.log2t = bs.log2t_global; s.max_ctas = 148 * 2; s.gtables = bs.gtables;
+  }
+  return s;
+}
+
+void free_bins(ptap_plan *p, BinSet &bs, cudaStream_t st) {
+  for (int q = 0; q < NBINS; ++q) pfree(p, bs.rows[q], st);
+  pfree(p, bs.gtables, st);
+  bs = BinSet{};
+}
+
+// mode: 0 all rows, 1 rows with P_o, 2 rows with P_d, 3 either
+ptap_status build_bins(ptap_plan *p, BinSet &bs, int64_t nrows, const int64_t *est, const int64_t *pd_rp,
+                       const int64_t *po_rp, int mode, bool num, int cat, cudaStream_t st) {
+  bs = BinSet{};
+  unsigned long long *cnt = p->d_u64;  // [0..3] counts, [4] selected
+  CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), st));
+  BinLists bl{};
+  bl.count = cnt;
+  CK(launch_bin_rows(nrows, est, pd_rp, po_rp, mode, bl, cnt + 4, st));
+  p->cnt.kernel_launches++;
+  unsigned long long h[8];
+  CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  bs.selected = (int64_t)h[4];
+  bool identity = (mode == 0 && (int64_t)h[0] == nrows);
+  if (identity) {
+    bs.identity0 = true;
+    bs.count[0] = nrows;
+  } else {
+    for (int q = 0; q < NBINS; ++q) {
+      bs.count[q] = (int64_t)h[q];
+      if (h[q]) CKS(palloc(p, &bs.rows[q], (int64_t)h[q], cat, st));
+    }
+    CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), st));
+    for (int q = 0; q < NBINS; ++q) bl.rows[q] = bs.rows[q];
+    CK(launch_bin_rows(nrows, est, pd_rp, po_rp, mode, bl, cnt + 4, st));
+    p->cnt.kernel_launches++;
+  }
+  if (bs.count[NBINS - 1] > 0) {
+    CK(cudaMemsetAsync(cnt + 5, 0, sizeof(unsigned long long), st));
+    CK(launch_max_est(bs.rows[NBINS - 1], (unsigned long long)bs.count[NBINS - 1], est, cnt + 5, st));
+    unsigned long long mx = 0;
+    CK(cudaMemcpyAsync(&mx, cnt + 5, sizeof(mx), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bs.log2t_global = ceil_log2(2 * (mx > 0 ? mx : 1));
+    LaunchShape s = shape_for(NBINS - 1, bs);
+    size_t bytes = (size_t)s.max_ctas * s.warps * row_kernel_group_bytes(bs.log2t_global, num);
+    CKS(palloc(p, &bs.gtables, (int64_t)bytes, cat, st));
+  }
+  return PTAP_OK;
+}
+
+template <typename F>
+ptap_status for_bins(ptap_plan *p, BinSet &bs, F launch) {
+  for (int q = 0; q < NBINS; ++q) {
+    if (bs.count[q] == 0) continue;
+    LaunchShape s = shape_for(q, bs);
+    const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
+    CK(launch(s, rows, (unsigned long long)bs.count[q]));
+    p->cnt.kernel_launches++;
+  }
+  return PTAP_OK;
+}
+
+// ---- arenas ------------------------------------------------------------------
+ptap_status arena_alloc(ptap_plan *p, Arena &ar, unsigned long long min_keys, cudaStream_t st) {
+  unsigned long long cap = 1024;
+  while (cap * 3 < min_keys * 4) cap <<= 1;  // <= 75% load at the estimate
+  CKS(palloc(p, &ar.keys, (int64_t)cap, CAT_TRANSIENT, st));
+  ar.mask = cap - 1;
+  CK(launch_arena_fill_empty(ar, st));
+  p->cnt.kernel_launches++;
+  return PTAP_OK;
+}
+
+ptap_status arena_grow(ptap_plan *p, Arena &ar, cudaStream_t st) {
+  Arena big{nullptr, 0};
+  CKS(arena_alloc(p, big, 2 * (ar.mask + 1), st));
+  CK(launch_arena_rehash(ar, big, p->d_status, st));
+  p->cnt.kernel_launches++;
+  pfree(p, ar.keys, st);
+  ar = big;
+  return PTAP_OK;
+}
+
+// Arena -> CSR over `nrows_dense` rows (row id = key / m), columns sorted.
+ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, int64_t **rp_out, int32_t **col_out,
+                         int64_t *nnz_out, int64_t **cnt_keep, cudaStream_t st) {
+  int64_t *cnt = nullptr, *rp = nullptr, *scratch = nullptr;
+  CKS(palloc(p, &cnt, nrows_dense, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nrows_dense > 0 ? nrows_dense : 1), st));
+  CK(launch_arena_rowcount(ar, p->m, cnt, st));
+  CKS(palloc(p, &rp, nrows_dense + 1, cat, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(nrows_dense), CAT_TRANSIENT, st));
+  CK(scan_exclusive(cnt, rp, nrows_dense, scratch, st));
+  int64_t nnz = 0;
+  CK(cudaMemcpyAsync(&nnz, rp + nrows_dense, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int32_t *col = nullptr;
+  CKS(palloc(p, &col, nnz, cat, st));
+  int64_t *cursor = scratch;  // reuse: needs nrows_dense entries
+  pfree(p, scratch, st);
+  CKS(palloc(p, &cursor, nrows_dense, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(cursor, 0, sizeof(int64_t) * (nrows_dense > 0 ? nrows_dense : 1), st));
+  CK(launch_arena_scatter(ar, p->m, rp, cursor, col, st));
+  pfree(p, cursor, st);
+  int32_t *wide = nullptr;
+  CKS(palloc(p, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(p->d_u64 + 6, 0, sizeof(unsigned long long), st));
+  CK(launch_sort_rows(nrows_dense, rp, col, nullptr, wide, p->d_u64 + 6, st));
+  unsigned long long nwide = 0;
+  CK(cudaMemcpyAsync(&nwide, p->d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(launch_sort_rows_block((int64_t)nwide, wide, rp, col, nullptr, p->d_status, st));
+  pfree(p, wide, st);
+  p->cnt.kernel_launches += 6;
+  if (cnt_keep) *cnt_keep = cnt; else pfree(p, cnt, st);
+  *rp_out = rp;
+  *col_out = col;
+  *nnz_out = nnz;
+  return PTAP_OK;
+}
+
+// send arena -> staging rows (global coarse ids, ascending) + CSR
+ptap_status arena_to_staging(ptap_plan *p, Arena ar, int cat, cudaStream_t st) {
+  int64_t *dense_rp = nullptr, *cnt = nullptr;
+  int32_t *col = nullptr;
+  int64_t nnz = 0;
+  CKS(arena_to_csr(p, ar, p->m, cat, &dense_rp, &col, &nnz, &cnt, st));
+  int64_t *flags = nullptr, *pos = nullptr, *scratch = nullptr;
+  CKS(palloc(p, &flags, p->m, CAT_TRANSIENT, st));
+  CKS(palloc(p, &pos, p->m + 1, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(p->m), CAT_TRANSIENT, st));
+  CK(launch_nonzero_flags(p->m, cnt, flags, st));
+  CK(scan_exclusive(flags, pos, p->m, scratch, st));
+  int64_t nrows = 0;
+  CK(cudaMemcpyAsync(&nrows, pos + p->m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CKS(palloc(p, &p->s_rows, nrows, cat, st));
+  CKS(palloc(p, &p->s_rp, nrows + 1, cat, st));
+  CK(launch_compact_rows(p->m, cnt, pos, dense_rp, p->s_rows, p->s_rp, st));
+  CK(cudaMemcpyAsync(p->s_rp + nrows, dense_rp + p->m, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  p->cnt.kernel_launches += 3;
+  pfree(p, flags, st);
+  pfree(p, pos, st);
+  pfree(p, scratch, st);
+  pfree(p, cnt, st);
+  pfree(p, dense_rp, st);
+  p->s_nrows = nrows;
+  p->s_nnz = nnz;
+  p->s_col = col;
+  CKS(palloc(p, &p->s_val, nnz, cat, st));
+  CK(cudaMemsetAsync(p->s_val, 0, sizeof(double) * (nnz > 0 ? nnz : 1), st));
+  return PTAP_OK;
+}
+
+ptap_status build_transpose(ptap_plan *p, Transpose &t, int64_t ntrows, const int64_t *rp, const int32_t *col,
+                            int64_t nnz, cudaStream_t st) {
+  t.nrows = ntrows;
+  t.nnz = nnz;
+  int64_t *cnt = nullptr, *scratch = nullptr;
+  CKS(palloc(p, &cnt, ntrows, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ntrows > 0 ? ntrows : 1), st));
+  if (nnz > 0) CK(launch_count_cols(nnz, col, cnt, st));
+  CKS(palloc(p, &t.rp, ntrows + 1, CAT_AUX, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(ntrows), CAT_TRANSIENT, st));
+  CK(scan_exclusive(cnt, t.rp, ntrows, scratch, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ntrows > 0 ? ntrows : 1), st));
+  CKS(palloc(p, &t.row, nnz, CAT_AUX, st));
+  CKS(palloc(p, &t.perm, nnz, CAT_PLAN, st));
+  CKS(palloc(p, &t.val, nnz, CAT_AUX, st));
+  if (nnz > 0) {
+    CK(launch_transpose_scatter(p->nloc, rp, col, t.rp, cnt, t.row, t.perm, st));
+    int32_t *wide = nullptr;
+    CKS(palloc(p, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st));
+    CK(cudaMemsetAsync(p->d_u64 + 6, 0, sizeof(unsigned long long), st));
+    CK(launch_sort_rows(ntrows, t.rp, t.row, t.perm, wide, p->d_u64 + 6, st));
+    unsigned long long nwide = 0;
+    CK(cudaMemcpyAsync(&nwide, p->d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(launch_sort_rows_block((int64_t)nwide, wide, t.rp, t.row, t.perm, p->d_status, st));
+    pfree(p, wide, st);
+  }
+  p->cnt.kernel_launches += 5;
+  pfree(p, cnt, st);
+  pfree(p, scratch, st);
+  return PTAP_OK;
+}
+
+ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStream_t st) {
+  int64_t *apub = nullptr, *ap_nnz = nullptr;
+  CKS(palloc(p, &apub, op.nloc, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(p->d_u64 + 7, 0, sizeof(unsigned long long), st));
+  CK(launch_row_work(op, apub, p->d_u64 + 7, st));
+  unsigned long long mac_ap = 0;
+  CK(cudaMemcpyAsync(&mac_ap, p->d_u64 + 7, sizeof(mac_ap), cudaMemcpyDeviceToHost, st));
+  BinSet tmp;
+  CKS(build_bins(p, tmp, op.nloc, apub, op.pd_rp, op.po_rp, 0, false, CAT_TRANSIENT, st));
+  p->cnt.mac_ap = (int64_t)mac_ap;
+  CKS(palloc(p, &ap_nnz, op.nloc, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(ap_nnz, 0, sizeof(int64_t) * (op.nloc > 0 ? op.nloc : 1), st));
+  CKS(for_bins(p, tmp, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+    return launch_ap_count(s, op, rows, n, ap_nnz, p->d_status, st);
+  }));
+  free_bins(p, tmp, st);
+  pfree(p, apub, st);
+  // bounds of the outer products
+  CK(cudaMemsetAsync(p->d_u64 + 8, 0, 3 * sizeof(unsigned long long), st));
+  CK(launch_outer_bounds(op.nloc, op.pd_rp, op.po_rp, ap_nnz, p->d_u64 + 8, st));
+  unsigned long long b[3];
+  CK(cudaMemcpyAsync(b, p->d_u64 + 8, sizeof(b), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->bound_local = b[0];
+  p->bound_send = b[1];
+  p->sum_ap = b[2];
+  p->cnt.mac_outer = (int64_t)(b[0] + b[1]);
+  p->cnt.kernel_launches += 3;
+  *ap_nnz_out = ap_nnz;
+  return PTAP_OK;
+}
+
+unsigned long long local_arena_estimate(const ptap_plan *p, int64_t extra) {
+  double avg = p->nloc > 0 ? (double)p->sum_ap / (double)p->nloc : 1.0;
+  double est = (double)p->ncl * (avg * 4.0 + 8.0) + (double)extra;
+  double bound = (double)p->bound_local + (double)extra;
+  if (est > bound) est = bound;
+  if (est < 64) est = 64;
+  return (unsigned long long)est;
+}
+
+// run `pass` until it completes without arena overflow (growing the arena)
+template <typename F>
+ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    CKS(pass());
+    int s = 0;
+    CKS(read_status(p, st, &s));
+    if (!(s & ST_ARENA_FULL)) {
+      if (s) return status_to_error(s, "symbolic");
+      return PTAP_OK;
+    }
+    CKS(arena_grow(p, ar, st));
+  }
+  return fail(PTAP_ERR_OOM, "symbolic arena kept overflowing");
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char *ptap_last_error(void) { return g_err.c_str(); }
+const char *ptap_version(void) { return "ptap_b200 0.1 (sm_100a)"; }
+
+ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan **out) {
+  if (!out) return fail(PTAP_ERR_VALUE, "null output");
+  if (algorithm < 0 || algorithm > 2) return fail(PTAP_ERR_VALUE, "unknown algorithm");
+  CKS(validate(ops));
+  ptap_plan *p = new ptap_plan();
+  p->alg = algorithm;
+  p->nloc = ops->n_local;
+  p->m = ops->m_global;
+  p->c_lo = ops->c_lo;
+  p->c_hi = ops->c_hi;
+  p->ncl = ops->c_hi - ops->c_lo;
+  p->colmap_len = ops->p_colmap_len;
+  cudaError_t e = cudaMalloc(&p->d_status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_u64, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(p->d_status, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(PTAP_ERR_CUDA, std::string("plan create: ") + cudaGetErrorString(e));
+  }
+  *out = p;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_destroy(ptap_plan *p) {
+  if (!p) return PTAP_OK;
+  cudaDeviceSynchronize();
+  for (auto &kv : p->allocs) cudaFree(kv.first);
+  cudaFree(p->d_status);
+  cudaFree(p->d_u64);
+  delete p;
+  return PTAP_OK;
+}
+
+ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *stream) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  CKS(validate(ops));
+  cudaStream_t st = (cudaStream_t)stream;
+  Ops op = make_ops(ops);
+  CKS(ap_sizes(p, op, &p->ap_nnz, st));
+  if (p->alg == PTAP_TWO_STEP) {
+    // C~ = A P (src/spgemm.py:184-202), booked as auxiliary
+    CKS(palloc(p, &p->ct_rp, p->nloc + 1, CAT_AUX, st));
+    int64_t *scratch = nullptr;
+    CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
+    CK(scan_exclusive(p->ap_nnz, p->ct_rp, p->nloc, scratch, st));
+    pfree(p, scratch, st);
+    CK(cudaMemcpyAsync(&p->ct_nnz, p->ct_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CKS(palloc(p, &p->ct_col, p->ct_nnz, CAT_AUX, st));
+    CKS(palloc(p, &p->ct_val, p->ct_nnz, CAT_AUX, st));
+    CKS(build_bins(p, p->bins_all, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 0, true, CAT_PLAN, st));
+    CKS(for_bins(p, p->bins_all, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ct_fill(s, op, rows, n, p->ct_rp, p->ct_col, p->d_status, st);
+    }));
+    int32_t *wide = nullptr;
+    CKS(palloc(p, &wide, p->ct_nnz / 1024 + 2, CAT_TRANSIENT, st));
+    CK(cudaMemsetAsync(p->d_u64 + 6, 0, sizeof(unsigned long long), st));
+    CK(launch_sort_rows(p->nloc, p->ct_rp, p->ct_col, nullptr, wide, p->d_u64 + 6, st));
+    unsigned long long nwide = 0;
+    CK(cudaMemcpyAsync(&nwide, p->d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(launch_sort_rows_block((int64_t)nwide, wide, p->ct_rp, p->ct_col, nullptr, p->d_status, st));
+    pfree(p, wide, st);
+    // explicit local transposes of P_d and P_o (src/tripleproduct.py:393-399)
+    CKS(build_transpose(p, p->ptd, p->ncl, op.pd_rp, op.pd_col, ops->p_diag.nnz, st));
+    CKS(build_transpose(p, p->pto, p->colmap_len, ops->p_off.row_ptr, ops->p_off.col, ops->p_off.nnz, st));
+    // send structure C_s = P_o^T C~ (no remote rows of C~ needed)
+    Arena send{nullptr, 0};
+    CKS(arena_alloc(p, send, p->bound_send + 16, st));
+    CKS(with_arena_retry(p, send, st, [&]() -> ptap_status {
+      CK(launch_ptc_symbolic(p->pto.nrows, p->pto.rp, p->pto.row, ops->p_colmap, 0, p->ct_rp, p->ct_col, send, p->m,
+                             p->d_status, st));
+      p->cnt.kernel_launches++;
+      return PTAP_OK;
+    }));
+    CKS(arena_to_staging(p, send, CAT_AUX, st));
+    pfree(p, send.keys, st);
+    p->cnt.symbolic_row_kernel_calls += p->nloc;
+  } else {
+    bool merged = p->alg == PTAP_MERGED;
+    if (merged) {
+      CKS(build_bins(p, p->bins_all, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 3, true, CAT_PLAN, st));
+      p->cnt.symbolic_row_kernel_calls += p->bins_all.selected;
+    } else {
+      CKS(build_bins(p, p->bins_send, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 1, true, CAT_PLAN, st));
+      CKS(build_bins(p, p->bins_local, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 2, true, CAT_PLAN, st));
+      p->cnt.symbolic_row_kernel_calls += p->bins_send.selected;
+    }
+    Arena send{nullptr, 0};
+    CKS(arena_alloc(p, send, p->bound_send + 16, st));
+    if (merged) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, 0), st));
+    BinSet &bs = merged ? p->bins_all : p->bins_send;
+    auto pass = [&]() -> ptap_status {
+      return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+        return launch_outer_symbolic(s, op, rows, n, 1, merged ? 1 : 0, p->local_arena, send, p->d_status, st);
+      });
+    };
+    if (merged) {
+      // the fused pass inserts into both arenas; grow the local one on overflow
+      for (int attempt = 0;; ++attempt) {
+        CKS(pass());
+        int s = 0;
+        CKS(read_status(p, st, &s));
+        if (!(s & ST_ARENA_FULL)) {
+          if (s) return status_to_error(s, "merged symbolic");
+          break;
+        }
+        if (attempt > 8) return fail(PTAP_ERR_OOM, "symbolic arena kept overflowing");
+        CKS(arena_grow(p, p->local_arena, st));
+        CKS(arena_grow(p, send, st));
+      }
+    } else {
+      CKS(with_arena_retry(p, send, st, pass));
+    }
+    CKS(arena_to_staging(p, send, CAT_PLAN, st));
+    pfree(p, send.keys, st);
+  }
+  int s = 0;
+  CKS(read_status(p, st, &s));
+  if (s) return status_to_error(s, "symbolic send");
+  p->cnt.nnz_staging = p->s_nnz;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_staging(ptap_plan *p, ptap_staging *out) {
+  if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
+  out->nrows = p->s_nrows;
+  out->nnz = p->s_nnz;
+  out->rows = p->s_rows;
+  out->row_ptr = p->s_rp;
+  out->col = p->s_col;
+  out->val = p->s_val;
+  return PTAP_OK;
+}
+
+ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const ptap_received *recv, void *stream) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  CKS(validate(ops));
+  cudaStream_t st = (cudaStream_t)stream;
+  Ops op = make_ops(ops);
+  int64_t rnnz = recv ? recv->nnz : 0;
+  if (p->alg != PTAP_MERGED) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st));
+  Arena &la = p->local_arena;
+  if (p->alg == PTAP_ALLATONCE) {
+    CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
+      return for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+        Arena none{nullptr, 0};
+        return launch_outer_symbolic(s, op, rows, n, 0, 1, la, none, p->d_status, st);
+      });
+    }));
+    p->cnt.symbolic_row_kernel_calls += p->bins_local.selected;
+  } else if (p->alg == PTAP_TWO_STEP) {
+    CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
+      CK(launch_ptc_symbolic(p->ptd.nrows, p->ptd.rp, p->ptd.row, nullptr, 0, p->ct_rp, p->ct_col, la, p->m,
+                             p->d_status, st));
+      p->cnt.kernel_launches++;
+      return PTAP_OK;
+    }));
+  }
+  // received structure (src/tripleproduct.py:191-200): owner rows only
+  p->r_src_nnz_off.clear();
+  p->r_nnz = rnnz;
+  if (recv && recv->nrows > 0) {
+    for (int k = 0; k <= recv->nsrc; ++k) p->r_src_nnz_off.push_back(recv->src_nnz_off[k]);
+    CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
+      CK(launch_arena_insert_batch(la, recv->nrows, recv->rows, recv->row_ptr, recv->col, p->m, p->c_lo, p->c_hi,
+                                   p->d_status, st));
+      p->cnt.kernel_launches++;
+      return PTAP_OK;
+    }));
+  }
+  // allocate C (src/tripleproduct.py:203-212, src/spgemm.py:71-104)
+  CKS(arena_to_csr(p, la, p->ncl, CAT_OUTPUT, &p->c_rp, &p->c_col, &p->c_nnz, nullptr, st));
+  pfree(p, la.keys, st);
+  la = Arena{nullptr, 0};
+  CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
+  CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
+  if (recv && recv->nrows > 0) {
+    CKS(palloc(p, &p->r_slot, rnnz, CAT_PLAN, st));
+    CK(launch_merge_slots(recv->nrows, recv->rows, recv->row_ptr, recv->col, p->c_lo, p->c_rp, p->c_col, p->r_slot,
+                          p->d_status, st));
+    p->cnt.kernel_launches++;
+  }
+  if (p->alg == PTAP_TWO_STEP) {
+    int64_t *est = nullptr;
+    CKS(palloc(p, &est, p->ncl > p->colmap_len ? p->ncl : p->colmap_len, CAT_TRANSIENT, st));
+    CK(launch_ptc_est(p->ptd.nrows, nullptr, 0, 0, p->ncl, nullptr, p->c_rp, est, st));
+    CKS(build_bins(p, p->bins_ptd, p->ptd.nrows, est, nullptr, nullptr, 0, true, CAT_PLAN, st));
+    CK(launch_ptc_est(p->pto.nrows, ops->p_colmap, 0, 1, p->s_nrows, p->s_rows, p->s_rp, est, st));
+    CKS(build_bins(p, p->bins_pto, p->pto.nrows, est, nullptr, nullptr, 0, true, CAT_PLAN, st));
+    pfree(p, est, st);
+    p->cnt.kernel_launches += 2;
+  }
+  pfree(p, p->ap_nnz, st);
+  int s = 0;
+  CKS(read_status(p, st, &s));
+  if (s & ST_DRIFT) {
+    if (recv && recv->nrows > 0)
+      return fail(PTAP_ERR_DRIFT, "received contribution rows outside the owned range or not in the structure");
+  }
+  if (s) return status_to_error(s, "symbolic local");
+  p->cnt.nnz_c = p->c_nnz;
+  p->cnt.symbolic_runs++;
+  p->symbolic_done = true;
+  return PTAP_OK;
+}
+
+static ptap_status numeric_ready(ptap_plan *p) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  if (p->released) return fail(PTAP_ERR_DRIFT, "plan internals were released (free-after-solve); rebuild the plan");
+  if (!p->symbolic_done) return fail(PTAP_ERR_VALUE, "numeric called before symbolic");
+  return PTAP_OK;
+}
+
+ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stream) {
+  CKS(numeric_ready(p));
+  cudaStream_t st = (cudaStream_t)stream;
+  Ops op = make_ops(ops);
+  if (p->alg == PTAP_TWO_STEP) {
+    CKS(for_bins(p, p->bins_all, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ct_numeric(s, op, rows, n, p->ct_rp, p->ct_col, p->ct_val, p->d_status, st);
+    }));
+    CK(launch_gather(p->ptd.nnz, p->ptd.perm, ops->p_diag.val, p->ptd.val, st));
+    CK(launch_gather(p->pto.nnz, p->pto.perm, ops->p_off.val, p->pto.val, st));
+    p->cnt.kernel_launches += 2;
+    PtcTarget tg{1, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+    CKS(for_bins(p, p->bins_pto, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ptc_numeric(s, rows, n, p->pto.rp, p->pto.row, p->pto.val, ops->p_colmap, 0, p->ct_rp,
+                                p->ct_col, p->ct_val, tg, p->d_status, st);
+    }));
+    return PTAP_OK;
+  }
+  bool merged = p->alg == PTAP_MERGED;
+  if (p->s_nnz > 0) CK(cudaMemsetAsync(p->s_val, 0, sizeof(double) * p->s_nnz, st));
+  if (merged && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
+  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+  BinSet &bs = merged ? p->bins_all : p->bins_send;
+  CKS(for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+    return launch_outer_numeric(s, op, rows, n, 1, merged ? 1 : 0, tg, p->d_status, st);
+  }));
+  p->cnt.numeric_row_kernel_calls += bs.selected;
+  return PTAP_OK;
+}
+
+ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *stream) {
+  CKS(numeric_ready(p));
+  cudaStream_t st = (cudaStream_t)stream;
+  Ops op = make_ops(ops);
+  if (p->alg == PTAP_TWO_STEP) {
+    PtcTarget tg{0, p->ncl, nullptr, p->c_rp, p->c_col, p->c_val};
+    CKS(for_bins(p, p->bins_ptd, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ptc_numeric(s, rows, n, p->ptd.rp, p->ptd.row, p->ptd.val, nullptr, 0, p->ct_rp, p->ct_col,
+                                p->ct_val, tg, p->d_status, st);
+    }));
+    p->cnt.numeric_row_kernel_calls += p->nloc;
+  } else if (p->alg == PTAP_ALLATONCE) {
+    if (p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
+    OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+    CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_outer_numeric(s, op, rows, n, 0, 1, tg, p->d_status, st);
+    }));
+    p->cnt.numeric_row_kernel_calls += p->bins_local.selected;
+  }
+  p->cnt.numeric_runs++;
+  return PTAP_OK;
+}
+
+ptap_status ptap_numeric_merge(ptap_plan *p, const double *recv_vals, void *stream) {
+  CKS(numeric_ready(p));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->r_nnz == 0) return PTAP_OK;
+  // ascending source rank, one launch per source (src/tripleproduct.py:215-229)
+  for (size_t k = 0; k + 1 < p->r_src_nnz_off.size(); ++k) {
+    int64_t a = p->r_src_nnz_off[k], b = p->r_src_nnz_off[k + 1];
+    if (b > a) {
+      CK(launch_merge_add(b - a, p->r_slot + a, recv_vals + a, p->c_val, st));
+      p->cnt.kernel_launches++;
+    }
+  }
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_check(ptap_plan *p, void *stream) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  int s = 0;
+  CKS(read_status(p, (cudaStream_t)stream, &s));
+  return status_to_error(s, "numeric");
+}
+
+ptap_status ptap_plan_get_c(ptap_plan *p, ptap_c_view *out) {
+  if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
+  out->nrows = p->ncl;
+  out->ncols = p->m;
+  out->nnz = p->c_nnz;
+  out->row_ptr = p->c_rp;
+  out->col = p->c_col;
+  out->val = p->c_val;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_release_cache(ptap_plan *p) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  if (p->released) return PTAP_OK;
+  cudaStream_t st = 0;
+  cudaDeviceSynchronize();
+  free_bins(p, p->bins_send, st);
+  free_bins(p, p->bins_local, st);
+  free_bins(p, p->bins_all, st);
+  free_bins(p, p->bins_ptd, st);
+  free_bins(p, p->bins_pto, st);
+  pfree(p, p->s_rows, st); pfree(p, p->s_rp, st); pfree(p, p->s_col, st); pfree(p, p->s_val, st);
+  pfree(p, p->r_slot, st);
+  pfree(p, p->ct_rp, st); pfree(p, p->ct_col, st); pfree(p, p->ct_val, st);
+  for (Transpose *t : {&p->ptd, &p->pto}) {
+    pfree(p, t->rp, st); pfree(p, t->row, st); pfree(p, t->perm, st); pfree(p, t->val, st);
+  }
+  cudaStreamSynchronize(st);
+  p->released = true;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_memory(ptap_plan *p, ptap_memory *out) {
+  if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
+  for (int c = 0; c < 5; ++c) {
+    out->current[c] = p->cur[c];
+    out->peak[c] = p->peak[c];
+  }
+  out->product_peak = p->prod_peak;
+  out->device_high_water = p->total_peak;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_counters(ptap_plan *p, ptap_counters *out) {
+  if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
+  *out = p->cnt;
+  return PTAP_OK;
+}
+
+// ---- standalone C~ = A P ------------------------------------------------------
+ptap_status ptap_spgemm_ap_symbolic(const ptap_operands *ops, int64_t *nnz_out, int64_t **row_ptr_out,
+                                    int32_t **col_out, void *stream) {
+  CKS(validate(ops));
+  cudaStream_t st = (cudaStream_t)stream;
+  ptap_plan tmp;
+  tmp.nloc = ops->n_local; tmp.m = ops->m_global; tmp.c_lo = ops->c_lo; tmp.c_hi = ops->c_hi;
+  if (cudaMalloc(&tmp.d_status, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tmp.d_u64, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(PTAP_ERR_CUDA, "alloc");
+  cudaMemset(tmp.d_status, 0, sizeof(int));
+  Ops op = make_ops(ops);
+  ptap_status rc = PTAP_OK;
+  int64_t *ap_nnz = nullptr, *rp = nullptr, *scratch = nullptr;
+  int32_t *col = nullptr, *wide = nullptr;
+  int64_t nnz = 0;
+  BinSet bs;
+  do {
+    if ((rc = ap_sizes(&tmp, op, &ap_nnz, st)) != PTAP_OK) break;
+    if (cudaMalloc(&rp, sizeof(int64_t) * (tmp.nloc + 1)) != cudaSuccess) { rc = fail(PTAP_ERR_OOM, "alloc"); break; }
+    if ((rc = palloc(&tmp, &scratch, scan_scratch_elems(tmp.nloc), CAT_TRANSIENT, st)) != PTAP_OK) break;
+    scan_exclusive(ap_nnz, rp, tmp.nloc, scratch, st);
+    cudaMemcpyAsync(&nnz, rp + tmp.nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (cudaMalloc(&col, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess) { rc = fail(PTAP_ERR_OOM, "alloc"); break; }
+    if ((rc = build_bins(&tmp, bs, tmp.nloc, ap_nnz, op.pd_rp, op.po_rp, 0, false, CAT_TRANSIENT, st)) != PTAP_OK) break;
+    rc = for_bins(&tmp, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ct_fill(s, op, rows, n, rp, col, tmp.d_status, st);
+    });
+    if (rc != PTAP_OK) break;
+    if ((rc = palloc(&tmp, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st)) != PTAP_OK) break;
+    cudaMemsetAsync(tmp.d_u64 + 6, 0, sizeof(unsigned long long), st);
+    launch_sort_rows(tmp.nloc, rp, col, nullptr, wide, tmp.d_u64 + 6, st);
+    unsigned long long nwide = 0;
+    cudaMemcpyAsync(&nwide, tmp.d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    launch_sort_rows_block((int64_t)nwide, wide, rp, col, nullptr, tmp.d_status, st);
+    int s = 0;
+    if ((rc = read_status(&tmp, st, &s)) != PTAP_OK) break;
+    if (s) rc = status_to_error(s, "spgemm symbolic");
+  } while (0);
+  cudaStreamSynchronize(st);
+  for (auto &kv : tmp.allocs) cudaFree(kv.first);
+  tmp.allocs.clear();
+  cudaFree(tmp.d_status);
+  cudaFree(tmp.d_u64);
+  tmp.d_status = nullptr;
+  tmp.d_u64 = nullptr;
+  if (rc != PTAP_OK) {
+    cudaFree(rp);
+    cudaFree(col);
+    return rc;
+  }
+  *nnz_out = nnz;
+  *row_ptr_out = rp;
+  *col_out = col;
+  return PTAP_OK;
+}
+
+ptap_status ptap_spgemm_ap_numeric(const ptap_operands *ops, const int64_t *row_ptr, const int32_t *col, double *val,
+                                   void *stream) {
+  CKS(validate(ops));
+  cudaStream_t st = (cudaStream_t)stream;
+  ptap_plan tmp;
+  tmp.nloc = ops->n_local; tmp.m = ops->m_global;
+  if (cudaMalloc(&tmp.d_status, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tmp.d_u64, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(PTAP_ERR_CUDA, "alloc");
+  cudaMemset(tmp.d_status, 0, sizeof(int));
+  Ops op = make_ops(ops);
+  ptap_status rc = PTAP_OK;
+  int64_t *est = nullptr;
+  BinSet bs;
+  do {
+    if ((rc = palloc(&tmp, &est, tmp.nloc, CAT_TRANSIENT, st)) != PTAP_OK) break;
+    launch_row_lengths(tmp.nloc, row_ptr, est, st);
+    if ((rc = build_bins(&tmp, bs, tmp.nloc, est, nullptr, nullptr, 0, true, CAT_TRANSIENT, st)) != PTAP_OK) break;
+    rc = for_bins(&tmp, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      return launch_ct_numeric(s, op, rows, n, row_ptr, col, val, tmp.d_status, st);
+    });
+    if (rc != PTAP_OK) break;
+    int s = 0;
+    if ((rc = read_status(&tmp, st, &s)) != PTAP_OK) break;
+    if (s) rc = status_to_error(s, "spgemm numeric");
+  } while (0);
+  cudaStreamSynchronize(st);
+  for (auto &kv : tmp.allocs) cudaFree(kv.first);
+  tmp.allocs.clear();
+  cudaFree(tmp.d_status);
+  cudaFree(tmp.d_u64);
+  tmp.d_status = nullptr;
+  tmp.d_u64 = nullptr;
+  return rc;
+}
+
+ptap_status ptap_device_free(void *ptr, void *stream) {
+  if (ptr) cudaFreeAsync(ptr, (cudaStream_t)stream);
+  return PTAP_OK;
+}
+
+ptap_status ptap_l2_flush(void *stream) {
+  static void *buf = nullptr;
+  const int64_t bytes = 512ll << 20;
+  if (!buf && cudaMalloc(&buf, bytes) != cudaSuccess) return fail(PTAP_ERR_OOM, "l2 flush buffer");
+  cudaError_t e = launch_touch(buf, bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(PTAP_ERR_CUDA, cudaGetErrorString(e));
+  return PTAP_OK;
+}
+
+}  // extern "C"

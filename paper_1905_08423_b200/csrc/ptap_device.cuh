@@ -1,0 +1,205 @@
+// ptap_device.cuh -- shared device-side pieces of the B200 PtAP library.
+//
+// Layout conventions:
+//   row offsets int64, column indices int32, values fp64; rows of every CSR
+//   keep ascending columns.  The C produced by the library is one CSR of the
+//   rank's coarse rows with GLOBAL columns (the diag/offdiag split of the
+//   reference's LocalMatrix is a host-side view taken on export).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ptap_b200.h"
+
+namespace ptapdev {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int32_t EMPTY32 = -1;
+constexpr unsigned long long EMPTY64 = 0xffffffffffffffffull;
+
+// Status bits set by kernels (read back by ptap_plan_check / symbolic).
+enum : int { ST_DRIFT = 1, ST_ARENA_FULL = 2, ST_TABLE_FULL = 4, ST_ROW_TOO_WIDE = 8 };
+
+// The operands one rank sees, flattened for kernels (see ptap_operands).
+struct Ops {
+  int64_t nloc, m, c_lo, c_hi;
+  const int64_t *ad_rp; const int32_t *ad_col; const double *ad_val;
+  const int64_t *ao_rp; const int32_t *ao_col; const double *ao_val;
+  const int64_t *pd_rp; const int32_t *pd_col; const double *pd_val;
+  const int64_t *po_rp; const int32_t *po_col; const double *po_val;
+  const int32_t *p_colmap;
+  const int64_t *pr_rp; const int32_t *pr_col; const double *pr_val;
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t hash32(uint32_t g, int log2t) {
+  return (g * 0x9E3779B1u) >> (32 - log2t);
+}
+__device__ __forceinline__ unsigned long long hash64(unsigned long long k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+  return k;
+}
+
+// first index in [lo,hi) with col[idx] >= g
+__device__ __forceinline__ int64_t lower_bound32(const int32_t *__restrict__ col, int64_t lo, int64_t hi, int32_t g) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(col + mid) < g) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int GROUP>
+__device__ __forceinline__ int group_sum(int v) {
+#pragma unroll
+  for (int o = GROUP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, GROUP);
+  return v;
+}
+
+// Insert / accumulate into an open-addressing table (keys int32, values
+// fp64) owned by one lane group.  Within one call of a step every lane of a
+// group carries a distinct key, so only the slot *claim* needs an atomic;
+// the value update is a plain read-modify-write.  The first product for a
+// key SETS the slot, later ones ADD (the reference's hm_add semantics,
+// src/_kernels.py:116-147), and products are rounded before the add.
+template <bool NUM>
+__device__ __forceinline__ bool table_put(int32_t *keys, double *vals, int log2t, int32_t g, double v, int &nnew) {
+  const uint32_t mask = (1u << log2t) - 1u;
+  uint32_t h = hash32((uint32_t)g, log2t);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    int32_t k = keys[h];
+    if (k == g) {
+      if (NUM) vals[h] = __dadd_rn(vals[h], v);
+      return true;
+    }
+    if (k == EMPTY32) {
+      int32_t old = atomicCAS(keys + h, EMPTY32, g);
+      if (old == EMPTY32) {
+        if (NUM) vals[h] = v;
+        ++nnew;
+        return true;
+      }
+      if (old == g) {  // cannot happen within a step (distinct keys); kept for safety
+        if (NUM) vals[h] = __dadd_rn(vals[h], v);
+        return true;
+      }
+    }
+    h = (h + 1) & mask;
+  }
+  return false;
+}
+
+__device__ __forceinline__ int table_find(const int32_t *keys, int log2t, int32_t g) {
+  const uint32_t mask = (1u << log2t) - 1u;
+  uint32_t h = hash32((uint32_t)g, log2t);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    int32_t k = keys[h];
+    if (k == g) return (int)h;
+    if (k == EMPTY32) return -1;
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+// Row i of A*P accumulated by one lane group of GROUP lanes, in the
+// reference's fold order (src/_kernels.py:205-227): the A_d entries of row i
+// in ascending order, then the A_o entries; for every A entry the whole P
+// row is scattered in one step (its columns are distinct, so the step is
+// conflict-free).  i < 0 marks an idle group (it still joins the shuffles).
+// Returns (per lane) the number of new keys this lane inserted.
+template <int GROUP, bool NUM>
+__device__ __forceinline__ int ap_row_accumulate(const Ops &op, int64_t i, int32_t *keys, double *vals,
+                                                 int log2t, int *status) {
+  const int gl = threadIdx.x & (GROUP - 1);
+  int nnew = 0;
+  bool ok = true;
+#pragma unroll 1
+  for (int src = 0; src < 2; ++src) {
+    const int64_t *arp = src ? op.ao_rp : op.ad_rp;
+    if (arp == nullptr) continue;  // uniform
+    const int32_t *acol = src ? op.ao_col : op.ad_col;
+    const double *aval = src ? op.ao_val : op.ad_val;
+    int64_t t0 = 0, t1 = 0;
+    if (i >= 0) { t0 = __ldg(arp + i); t1 = __ldg(arp + i + 1); }
+    int len = (int)(t1 - t0);
+    int maxlen = __reduce_max_sync(FULL, len);
+#pragma unroll 1
+    for (int tb = 0; tb < maxlen; tb += GROUP) {
+      // each lane of the group preloads one A entry and its P row bounds
+      int t = tb + gl;
+      double a = 0.0;
+      int64_t d0 = 0, d1 = 0, o0 = 0, o1 = 0;
+      if (t < len) {
+        int32_t k = __ldg(acol + t0 + t);
+        if (NUM) a = __ldg(aval + t0 + t);
+        if (src == 0) {
+          d0 = __ldg(op.pd_rp + k); d1 = __ldg(op.pd_rp + k + 1);
+          if (op.po_rp) { o0 = __ldg(op.po_rp + k); o1 = __ldg(op.po_rp + k + 1); }
+        } else {
+          d0 = __ldg(op.pr_rp + k); d1 = __ldg(op.pr_rp + k + 1);
+        }
+      }
+      int steps = min(GROUP, maxlen - tb);
+#pragma unroll 1
+      for (int j = 0; j < steps; ++j) {
+        double aj = __shfl_sync(FULL, a, j, GROUP);
+        int64_t sd0 = __shfl_sync(FULL, d0, j, GROUP), sd1 = __shfl_sync(FULL, d1, j, GROUP);
+        int64_t so0 = __shfl_sync(FULL, o0, j, GROUP), so1 = __shfl_sync(FULL, o1, j, GROUP);
+        int nd = (int)(sd1 - sd0);
+        int plen = nd + (int)(so1 - so0);
+        if (tb + j >= len) plen = 0;
+        for (int u = gl; u < plen; u += GROUP) {
+          int32_t g;
+          double p = 0.0;
+          if (u < nd) {
+            if (src == 0) { g = __ldg(op.pd_col + sd0 + u) + (int32_t)op.c_lo; if (NUM) p = __ldg(op.pd_val + sd0 + u); }
+            else { g = __ldg(op.pr_col + sd0 + u); if (NUM) p = __ldg(op.pr_val + sd0 + u); }
+          } else {
+            int64_t e = so0 + (u - nd);
+            g = __ldg(op.p_colmap + __ldg(op.po_col + e));
+            if (NUM) p = __ldg(op.po_val + e);
+          }
+          ok &= table_put<NUM>(keys, vals, log2t, g, NUM ? __dmul_rn(aj, p) : 0.0, nnew);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (!ok) atomicOr(status, ST_TABLE_FULL);
+  return nnew;
+}
+
+// Compact a group's table into (key, value) lists; returns the entry count
+// (uniform within the group).  Order is slot order (irrelevant downstream).
+template <int GROUP, bool NUM>
+__device__ __forceinline__ int table_compact(const int32_t *keys, const double *vals, int tsize,
+                                             int32_t *lk, double *lv) {
+  const int lane = lane_id();
+  const int gl = lane & (GROUP - 1);
+  const unsigned gmask = (GROUP == 32) ? FULL : (((1u << GROUP) - 1u) << (lane & ~(GROUP - 1)));
+  int n = 0;
+  for (int s0 = 0; s0 < tsize; s0 += GROUP) {
+    int s = s0 + gl;
+    int32_t k = keys[s];
+    bool occ = k != EMPTY32;
+    unsigned b = __ballot_sync(FULL, occ) & gmask;
+    int before = __popc(b & ((1u << lane) - 1u));
+    if (occ) {
+      lk[n + before] = k;
+      if (NUM) lv[n + before] = vals[s];
+    }
+    n += __popc(b);
+  }
+  __syncwarp();
+  return n;
+}
+
+template <int GROUP>
+__device__ __forceinline__ void table_clear(int32_t *keys, int tsize) {
+  const int gl = threadIdx.x & (GROUP - 1);
+  for (int s = gl; s < tsize; s += GROUP) keys[s] = EMPTY32;
+  __syncwarp();
+}
+
+}  // namespace ptapdev

@@ -1,0 +1,1015 @@
+// ptap_kernels.cu -- sm_100a kernels of the B200 PtAP library.
+//
+// Kernel map (reference function each one replaces, /root/reference/pkg/src/ptap):
+//   k_row_work            work estimates for binning (AP-row upper bound)    (new)
+//   k_bin_rows            rows -> work bins                                  (new)
+//   k_ap_count<G>         exact nnz of AP rows                               _kernels.py:178-202 row_ap_symbolic
+//   k_outer_symbolic<G>   structural outer products into combined-key arenas _kernels.py:361-418 outer_symbolic_driver
+//   k_arena_*             sorted drain of an arena into CSR rows             tripleproduct.py:165-212
+//   k_sort_rows*          per-row sort of columns (optionally with payload)  hs_drain / np.sort
+//   k_outer_numeric<G>    fused AP row + outer-product scatter               _kernels.py:446-515 outer_numeric_driver
+//   k_merge_slots/add     received batches -> C in ascending source order    _kernels.py:528-548 scatter_add_rows
+//   k_ct_fill/numeric<G>  two-step C~ = A P rows                             _kernels.py:248-349 ap_{symbolic,numeric}_driver
+//   k_transpose_*         stable transpose of P blocks with permutation      sparse.py:165-178
+//   k_ptc_symbolic        two-step P^T C~ structure                          _kernels.py:558-580
+//   k_ptc_numeric<G>      two-step P^T C~ values (staging or C)              _kernels.py:583-677
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ptap_device.cuh"
+#include "ptap_kernels.cuh"
+
+namespace ptapdev {
+
+// ---------------------------------------------------------------------------
+// work estimates: apub(i) = sum over A row i of nnz(P row k); mac_ap total
+// ---------------------------------------------------------------------------
+__global__ void k_row_work(Ops op, int64_t *apub, unsigned long long *mac_total) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long mine = 0;
+  if (i < op.nloc) {
+    int64_t s = 0;
+    for (int64_t t = op.ad_rp[i]; t < op.ad_rp[i + 1]; ++t) {
+      int32_t k = op.ad_col[t];
+      s += op.pd_rp[k + 1] - op.pd_rp[k];
+      if (op.po_rp) s += op.po_rp[k + 1] - op.po_rp[k];
+    }
+    if (op.ao_rp)
+      for (int64_t t = op.ao_rp[i]; t < op.ao_rp[i + 1]; ++t) {
+        int32_t k = op.ao_col[t];
+        s += op.pr_rp[k + 1] - op.pr_rp[k];
+      }
+    apub[i] = s;
+    mine = (unsigned long long)s;
+  }
+  unsigned long long w = mine;
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(FULL, w, o);
+  if (lane_id() == 0 && w) atomicAdd(mac_total, w);
+}
+
+// rows -> bins by estimated distinct keys; mode selects rows like the
+// reference's loop predicates (0 all, 1 P_o nonempty, 2 P_d nonempty, 3 either)
+__global__ void k_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_rp, const int64_t *po_rp,
+                           int mode, BinLists bl, unsigned long long *selected) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int b = -1;
+  if (i < nrows) {
+    bool pd = pd_rp && pd_rp[i + 1] > pd_rp[i];
+    bool po = po_rp && po_rp[i + 1] > po_rp[i];
+    bool want = mode == 0 || (mode == 1 && po) || (mode == 2 && pd) || (mode == 3 && (po || pd));
+    if (want) {
+      int64_t n = est[i];
+      b = NBINS - 1;
+      for (int q = 0; q < NBINS - 1; ++q)
+        if (n <= bin_capacity(q)) { b = q; break; }
+    }
+  }
+  const int lane = lane_id();
+  unsigned any = __ballot_sync(FULL, b >= 0);
+  if (lane == 0 && any) atomicAdd(selected, (unsigned long long)__popc(any));
+  for (int q = 0; q < NBINS; ++q) {
+    unsigned bits = __ballot_sync(FULL, b == q);
+    if (!bits) continue;
+    int leader = __ffs(bits) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(bl.count + q, (unsigned long long)__popc(bits));
+    base = __shfl_sync(FULL, base, leader);
+    if (b == q && bl.rows[q]) bl.rows[q][base + __popc(bits & ((1u << lane) - 1u))] = (int32_t)i;
+  }
+}
+
+// max estimate inside the last (global-table) bin
+__global__ void k_max_est(const int32_t *rows, unsigned long long nrows, const int64_t *est, unsigned long long *mx) {
+  unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (r < nrows) v = (unsigned long long)est[rows ? rows[r] : (int32_t)r];
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  if (lane_id() == 0 && v) atomicMax(mx, v);
+}
+
+// ---------------------------------------------------------------------------
+// group-table addressing shared by the row kernels
+// ---------------------------------------------------------------------------
+struct GroupTables {
+  int32_t *keys; double *vals; int32_t *lk; double *lv;
+};
+// per-group footprint: vals[T] lv[T/2] (fp64) then keys[T] lk[T/2] (int32)
+__host__ __device__ inline size_t group_bytes(int log2t, bool num) {
+  size_t T = (size_t)1 << log2t;
+  return num ? (T * 8 + (T / 2) * 8 + T * 4 + (T / 2) * 4) : (T * 4 + (T / 2) * 4);
+}
+template <int GROUP, bool NUM>
+__device__ __forceinline__ GroupTables group_tables(unsigned char *gtables, int log2t) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int gpw = 32 / GROUP;
+  const int gid = (threadIdx.x >> 5) * gpw + lane_id() / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  size_t gb = group_bytes(log2t, NUM);
+  unsigned char *base = gtables ? gtables + ((size_t)blockIdx.x * gpc + gid) * gb : smem + (size_t)gid * gb;
+  const int T = 1 << log2t;
+  GroupTables t;
+  if (NUM) {
+    t.vals = (double *)base; t.lv = t.vals + T;
+    t.keys = (int32_t *)(t.lv + T / 2); t.lk = t.keys + T;
+  } else {
+    t.vals = nullptr; t.lv = nullptr;
+    t.keys = (int32_t *)base; t.lk = t.keys + T;
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// exact AP row sizes
+// ---------------------------------------------------------------------------
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_ap_count(Ops op, const int32_t *rows, unsigned long long nrows, int log2t,
+                                                  unsigned char *gtables, int64_t *ap_nnz, int *status) {
+  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    table_clear<GROUP>(tb.keys, T);
+    int nnew = ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    nnew = group_sum<GROUP>(nnew);
+    if (i >= 0 && (lane_id() & (GROUP - 1)) == 0) ap_nnz[i] = nnew;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// arenas
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void arena_insert(unsigned long long *ar, unsigned long long mask, unsigned long long key,
+                                             int *status) {
+  unsigned long long h = hash64(key) & mask;
+  for (int probe = 0; probe < 8192; ++probe) {
+    unsigned long long k = ar[h];
+    if (k == key) return;
+    if (k == EMPTY64) {
+      unsigned long long old = atomicCAS(ar + h, EMPTY64, key);
+      if (old == EMPTY64 || old == key) return;
+    }
+    h = (h + 1) & mask;
+  }
+  atomicOr(status, ST_ARENA_FULL);
+}
+
+// structural outer products P(i,:) (x) AP(i,:) (src/_kernels.py:361-418):
+// local rows go to the local arena keyed (J - c_lo)*m + g, send rows to the
+// send arena keyed J*m + g.
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                        int log2t, unsigned char *gtables, int do_send,
+                                                        int do_local, Arena local, Arena send, int *status) {
+  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  const unsigned long long m = (unsigned long long)op.m;
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    int64_t pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
+    if (i >= 0) {
+      pd0 = op.pd_rp[i]; pd1 = op.pd_rp[i + 1];
+      if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
+    }
+    bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
+    if (!(wl || ws)) i = -1;
+    table_clear<GROUP>(tb.keys, T);
+    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    int n = table_compact<GROUP, false>(tb.keys, nullptr, T, tb.lk, nullptr);
+    if (i >= 0 && n > 0) {
+      if (wl) {
+        int tot = (int)(pd1 - pd0) * n;
+        for (int f = gl; f < tot; f += GROUP) {
+          int jj = f / n, e = f - jj * n;
+          unsigned long long J = (unsigned long long)op.pd_col[pd0 + jj];
+          arena_insert(local.keys, local.mask, J * m + (unsigned long long)tb.lk[e], status);
+        }
+      }
+      if (ws) {
+        int tot = (int)(po1 - po0) * n;
+        for (int f = gl; f < tot; f += GROUP) {
+          int jj = f / n, e = f - jj * n;
+          unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[po0 + jj]];
+          arena_insert(send.keys, send.mask, J * m + (unsigned long long)tb.lk[e], status);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_arena_fill_empty(unsigned long long *ar, unsigned long long cap) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < cap) ar[s] = EMPTY64;
+}
+
+// received (row, col) structure into the local arena (src/_kernels.py:518-525)
+__global__ void k_arena_insert_batch(Arena ar, int64_t nrows, const int32_t *rows, const int64_t *rp,
+                                     const int32_t *col, int64_t m, int64_t c_lo, int64_t c_hi, int *status) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nrows) return;
+  int32_t J = rows[w];
+  if (J < c_lo || J >= c_hi) { if (lane_id() == 0) atomicOr(status, ST_DRIFT); return; }
+  unsigned long long base = (unsigned long long)(J - c_lo) * (unsigned long long)m;
+  for (int64_t e = rp[w] + lane_id(); e < rp[w + 1]; e += 32)
+    arena_insert(ar.keys, ar.mask, base + (unsigned long long)col[e], status);
+}
+
+__global__ void k_arena_rowcount(Arena ar, unsigned long long m, int64_t *cnt) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > ar.mask) return;
+  unsigned long long k = ar.keys[s];
+  if (k != EMPTY64) atomicAdd((unsigned long long *)(cnt + k / m), 1ull);
+}
+
+__global__ void k_arena_scatter(Arena ar, unsigned long long m, const int64_t *rp, int64_t *cursor, int32_t *col) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > ar.mask) return;
+  unsigned long long k = ar.keys[s];
+  if (k == EMPTY64) return;
+  unsigned long long r = k / m;
+  unsigned long long pos = (unsigned long long)rp[r] + atomicAdd((unsigned long long *)(cursor + r), 1ull);
+  col[pos] = (int32_t)(k - r * m);
+}
+
+// ---------------------------------------------------------------------------
+// per-row sorts (warp per row, bitonic in shared memory, <= 1024 entries;
+// block per row up to 8192 entries for the rare wide rows)
+// ---------------------------------------------------------------------------
+template <bool PAIRS>
+__global__ void __launch_bounds__(256) k_sort_rows(int64_t nrows, const int64_t *rp, int32_t *keys,
+                                                   int64_t *payload, int32_t *wide_rows,
+                                                   unsigned long long *nwide) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int wpc = blockDim.x >> 5;
+  int32_t *sk = (int32_t *)(smem + (size_t)warp * 1024 * 4);
+  int64_t *sp = (int64_t *)(smem + (size_t)wpc * 1024 * 4 + (size_t)warp * 1024 * 8);
+  for (int64_t r = (int64_t)blockIdx.x * wpc + warp; r < nrows; r += (int64_t)gridDim.x * wpc) {
+    int64_t b = rp[r];
+    int L = (int)(rp[r + 1] - b);
+    if (L <= 1) continue;
+    if (L > 1024) {
+      if (lane == 0) wide_rows[atomicAdd(nwide, 1ull)] = (int32_t)r;
+      continue;
+    }
+    int P2 = 1;
+    while (P2 < L) P2 <<= 1;
+    for (int x = lane; x < P2; x += 32) {
+      sk[x] = x < L ? keys[b + x] : INT32_MAX;
+      if (PAIRS) sp[x] = x < L ? payload[b + x] : 0;
+    }
+    __syncwarp();
+    for (int k = 2; k <= P2; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int x = lane; x < P2; x += 32) {
+          int y = x ^ j;
+          if (y > x) {
+            bool up = (x & k) == 0;
+            int32_t kx = sk[x], ky = sk[y];
+            if ((kx > ky) == up) {
+              sk[x] = ky; sk[y] = kx;
+              if (PAIRS) { int64_t t = sp[x]; sp[x] = sp[y]; sp[y] = t; }
+            }
+          }
+        }
+        __syncwarp();
+      }
+    for (int x = lane; x < L; x += 32) {
+      keys[b + x] = sk[x];
+      if (PAIRS) payload[b + x] = sp[x];
+    }
+    __syncwarp();
+  }
+}
+
+template <bool PAIRS>
+__global__ void __launch_bounds__(1024) k_sort_rows_block(const int32_t *rows, const int64_t *rp, int32_t *keys,
+                                                          int64_t *payload, int *status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t r = rows[blockIdx.x];
+  int64_t b = rp[r];
+  int L = (int)(rp[r + 1] - b);
+  if (L > 8192) { if (threadIdx.x == 0) atomicOr(status, ST_ROW_TOO_WIDE); return; }
+  int P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  int32_t *sk = (int32_t *)smem;
+  int64_t *sp = (int64_t *)(smem + 8192 * 4);
+  for (int x = threadIdx.x; x < P2; x += blockDim.x) {
+    sk[x] = x < L ? keys[b + x] : INT32_MAX;
+    if (PAIRS) sp[x] = x < L ? payload[b + x] : 0;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int x = threadIdx.x; x < P2; x += blockDim.x) {
+        int y = x ^ j;
+        if (y > x) {
+          bool up = (x & k) == 0;
+          int32_t kx = sk[x], ky = sk[y];
+          if ((kx > ky) == up) {
+            sk[x] = ky; sk[y] = kx;
+            if (PAIRS) { int64_t t = sp[x]; sp[x] = sp[y]; sp[y] = t; }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int x = threadIdx.x; x < L; x += blockDim.x) {
+    keys[b + x] = sk[x];
+    if (PAIRS) payload[b + x] = sp[x];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused numeric all-at-once / merged (src/_kernels.py:446-515)
+// ---------------------------------------------------------------------------
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_outer_numeric(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                       int log2t, unsigned char *gtables, int do_send,
+                                                       int do_local, OuterTargets tg, int *status) {
+  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    int64_t pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
+    if (i >= 0) {
+      pd0 = op.pd_rp[i]; pd1 = op.pd_rp[i + 1];
+      if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
+    }
+    bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
+    if (!(wl || ws)) i = -1;
+    if (__all_sync(FULL, i < 0)) continue;
+    table_clear<GROUP>(tb.keys, T);
+    ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, status);
+    int n = table_compact<GROUP, true>(tb.keys, tb.vals, T, tb.lk, tb.lv);
+    if (i >= 0 && n > 0) {
+      if (wl) {
+        int tot = (int)(pd1 - pd0) * n;
+        for (int f = gl; f < tot; f += GROUP) {
+          int jj = f / n, e = f - jj * n;
+          int32_t J = __ldg(op.pd_col + pd0 + jj);
+          double pij = __ldg(op.pd_val + pd0 + jj);
+          int32_t g = tb.lk[e];
+          int64_t c0 = __ldg(tg.c_rp + J), c1 = __ldg(tg.c_rp + J + 1);
+          int64_t pos = lower_bound32(tg.c_col, c0, c1, g);
+          if (pos < c1 && __ldg(tg.c_col + pos) == g) atomicAdd(tg.c_val + pos, __dmul_rn(pij, tb.lv[e]));
+          else atomicOr(status, ST_DRIFT);
+        }
+      }
+      if (ws) {
+        int tot = (int)(po1 - po0) * n;
+        for (int f = gl; f < tot; f += GROUP) {
+          int jj = f / n, e = f - jj * n;
+          int32_t Jg = __ldg(op.p_colmap + __ldg(op.po_col + po0 + jj));
+          double pij = __ldg(op.po_val + po0 + jj);
+          int32_t g = tb.lk[e];
+          int64_t sr = lower_bound32(tg.s_rows, 0, tg.s_nrows, Jg);
+          if (sr >= tg.s_nrows || __ldg(tg.s_rows + sr) != Jg) { atomicOr(status, ST_DRIFT); continue; }
+          int64_t c0 = __ldg(tg.s_rp + sr), c1 = __ldg(tg.s_rp + sr + 1);
+          int64_t pos = lower_bound32(tg.s_col, c0, c1, g);
+          if (pos < c1 && __ldg(tg.s_col + pos) == g) atomicAdd(tg.s_val + pos, __dmul_rn(pij, tb.lv[e]));
+          else atomicOr(status, ST_DRIFT);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// received batches: slot map (symbolic) and ordered adds (numeric)
+// ---------------------------------------------------------------------------
+__global__ void k_merge_slots(int64_t nrows, const int32_t *rows, const int64_t *rp, const int32_t *col,
+                              int64_t c_lo, const int64_t *c_rp, const int32_t *c_col, int64_t *slot, int *status) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nrows) return;
+  int64_t J = rows[w] - c_lo;
+  int64_t c0 = c_rp[J], c1 = c_rp[J + 1];
+  for (int64_t e = rp[w] + lane_id(); e < rp[w + 1]; e += 32) {
+    int64_t pos = lower_bound32(c_col, c0, c1, col[e]);
+    if (pos < c1 && c_col[pos] == col[e]) slot[e] = pos;
+    else { slot[e] = -1; atomicOr(status, ST_DRIFT); }
+  }
+}
+
+__global__ void k_merge_add(int64_t n, const int64_t *slot, const double *vals, double *c_val) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) {
+    int64_t s = slot[e];
+    if (s >= 0) c_val[s] = __dadd_rn(c_val[s], vals[e]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// two-step: C~ = A P rows (structure sorted later), values onto structure
+// ---------------------------------------------------------------------------
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_ct_fill(Ops op, const int32_t *rows, unsigned long long nrows, int log2t,
+                                                 unsigned char *gtables, const int64_t *ct_rp, int32_t *ct_col,
+                                                 int *status) {
+  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    table_clear<GROUP>(tb.keys, T);
+    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    int n = table_compact<GROUP, false>(tb.keys, nullptr, T, tb.lk, nullptr);
+    if (i >= 0) {
+      int64_t b = ct_rp[i];
+      if (ct_rp[i + 1] - b != n) { if (gl == 0) atomicOr(status, ST_DRIFT); }
+      else for (int e = gl; e < n; e += GROUP) ct_col[b + e] = tb.lk[e];
+    }
+    __syncwarp();
+  }
+}
+
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_ct_numeric(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                    int log2t, unsigned char *gtables, const int64_t *ct_rp,
+                                                    const int32_t *ct_col, double *ct_val, int *status) {
+  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    table_clear<GROUP>(tb.keys, T);
+    int nnew = ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, status);
+    nnew = group_sum<GROUP>(nnew);
+    if (i >= 0) {
+      int64_t b = ct_rp[i], L = ct_rp[i + 1] - b;
+      if (L != nnew) { if (gl == 0) atomicOr(status, ST_DRIFT); }
+      else
+        for (int64_t e = gl; e < L; e += GROUP) {
+          int s = table_find(tb.keys, log2t, ct_col[b + e]);
+          if (s < 0) atomicOr(status, ST_DRIFT);
+          else ct_val[b + e] = tb.vals[s];
+        }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stable transpose of a P block (src/sparse.py:165-178)
+// ---------------------------------------------------------------------------
+__global__ void k_count_cols(int64_t nnz, const int32_t *col, int64_t *cnt) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) atomicAdd((unsigned long long *)(cnt + col[e]), 1ull);
+}
+
+__global__ void k_transpose_scatter(int64_t nrows, const int64_t *rp, const int32_t *col, const int64_t *t_rp,
+                                    int64_t *cursor, int32_t *t_row, int64_t *t_perm) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+    int32_t q = col[e];
+    int64_t pos = t_rp[q] + (int64_t)atomicAdd((unsigned long long *)(cursor + q), 1ull);
+    t_row[pos] = (int32_t)i;
+    t_perm[pos] = e;
+  }
+}
+
+__global__ void k_gather(int64_t n, const int64_t *perm, const double *src, double *dst) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) dst[e] = src[perm[e]];
+}
+
+// two-step structure of P^T C~ rows into an arena; target_map maps the
+// transposed row id to the arena row (local J, or global J for the send side)
+__global__ void k_ptc_symbolic(int64_t nrows, const int64_t *t_rp, const int32_t *t_row, const int32_t *target_map,
+                               int64_t target_offset, const int64_t *ct_rp, const int32_t *ct_col, Arena ar,
+                               unsigned long long m, int *status) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nrows) return;
+  unsigned long long tgt = target_map ? (unsigned long long)target_map[w] : (unsigned long long)(w + target_offset);
+  for (int64_t t = t_rp[w]; t < t_rp[w + 1]; ++t) {
+    int32_t i = t_row[t];
+    for (int64_t e = ct_rp[i] + lane_id(); e < ct_rp[i + 1]; e += 32)
+      arena_insert(ar.keys, ar.mask, tgt * m + (unsigned long long)ct_col[e], status);
+  }
+}
+
+// two-step numeric rows of P^T C~ (src/_kernels.py:583-677): fold over the
+// transposed row's entries (ascending fine row) with C~ rows scattered per
+// step; then written onto the target structure (staging: set; C: 0 + acc).
+template <int GROUP>
+__global__ void __launch_bounds__(256) k_ptc_numeric(const int32_t *rows, unsigned long long nrows, int log2t,
+                                                     unsigned char *gtables, const int64_t *t_rp,
+                                                     const int32_t *t_row, const double *t_val,
+                                                     const int32_t *target_map, int64_t target_offset,
+                                                     const int64_t *ct_rp, const int32_t *ct_col,
+                                                     const double *ct_val, PtcTarget tg, int *status) {
+  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t q = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    table_clear<GROUP>(tb.keys, T);
+    int64_t t0 = 0, t1 = 0;
+    if (q >= 0) { t0 = t_rp[q]; t1 = t_rp[q + 1]; }
+    int len = (int)(t1 - t0);
+    int maxlen = __reduce_max_sync(FULL, len);
+    bool ok = true;
+    int nnew = 0;
+    for (int t = 0; t < maxlen; ++t) {
+      int64_t e0 = 0, e1 = 0;
+      double lv = 0.0;
+      if (t < len) {
+        int32_t i = t_row[t0 + t];
+        lv = t_val[t0 + t];
+        e0 = ct_rp[i]; e1 = ct_rp[i + 1];
+      }
+      for (int64_t e = e0 + gl; e < e1; e += GROUP)
+        ok &= table_put<true>(tb.keys, tb.vals, log2t, ct_col[e], __dmul_rn(lv, ct_val[e]), nnew);
+      __syncwarp();
+    }
+    if (!ok) atomicOr(status, ST_TABLE_FULL);
+    nnew = group_sum<GROUP>(nnew);
+    if (q >= 0) {
+      int64_t tgt = target_map ? (int64_t)target_map[q] : q + target_offset;
+      int64_t r = tgt;
+      if (tg.is_staging) {
+        r = lower_bound32(tg.rows, 0, tg.nrows, (int32_t)tgt);
+        if (r >= tg.nrows || tg.rows[r] != (int32_t)tgt) r = -1;
+      }
+      if (r < 0) {
+        if (nnew > 0 && gl == 0) atomicOr(status, ST_DRIFT);
+      } else {
+        int64_t c0 = tg.rp[r], c1 = tg.rp[r + 1];
+        int found = 0;
+        for (int64_t e = c0 + gl; e < c1; e += GROUP) {
+          int s = table_find(tb.keys, log2t, tg.col[e]);
+          if (s >= 0) {
+            ++found;
+            tg.val[e] = tg.is_staging ? tb.vals[s] : __dadd_rn(0.0, tb.vals[s]);
+          } else {
+            tg.val[e] = 0.0;  // C slot fed only by received batches (or drift on staging)
+            if (tg.is_staging) atomicOr(status, ST_DRIFT);
+          }
+        }
+        found = group_sum<GROUP>(found);
+        if (found != nnew && gl == 0) atomicOr(status, ST_DRIFT);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scans (exclusive, int64), compaction helpers
+// ---------------------------------------------------------------------------
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tiles(const int64_t *in, int64_t *out, int64_t n,
+                                                             int64_t *tile_sums) {
+  __shared__ int64_t warp_tot[SCAN_THREADS / 32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int64_t v[SCAN_ITEMS];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0;
+    s += v[k];
+  }
+  int64_t incl = s;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t wt = lane < SCAN_THREADS / 32 ? warp_tot[lane] : 0;
+    int64_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < SCAN_THREADS / 32) warp_tot[lane] = wi - wt;
+    if (lane == SCAN_THREADS / 32 - 1) tile_sums[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  int64_t run = warp_tot[warp] + incl - s;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+}
+
+__global__ void k_scan_add(int64_t *out, int64_t n, const int64_t *tile_off) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) out[e] += tile_off[e / SCAN_TILE];
+}
+
+__global__ void k_set_total(int64_t *out, int64_t n, const int64_t *in) {
+  // out[n] = out[n-1] + in[n-1]
+  if (n == 0) out[0] = 0;
+  else out[n] = out[n - 1] + in[n - 1];
+}
+
+// flags[i] = cnt[i] > 0 ; used to compact the nonempty send rows in order
+__global__ void k_nonzero_flags(int64_t n, const int64_t *cnt, int64_t *flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = cnt[i] > 0 ? 1 : 0;
+}
+
+__global__ void k_compact_rows(int64_t n, const int64_t *cnt, const int64_t *pos, const int64_t *dense_rp,
+                               int32_t *rows, int64_t *rp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && cnt[i] > 0) {
+    rows[pos[i]] = (int32_t)i;
+    rp[pos[i]] = dense_rp[i];
+  }
+}
+
+__global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_iota32(int32_t *p, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int32_t)i;
+}
+
+__global__ void k_colmap_targets(int64_t n, const int32_t *colmap, int32_t *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = colmap[i];
+}
+
+__global__ void k_row_lengths(int64_t n, const int64_t *rp, int64_t *len) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) len[i] = rp[i + 1] - rp[i];
+}
+
+// outer-product bounds: out[0] = sum nnz(P_d(i,:))*ap_nnz(i), out[1] = sum
+// nnz(P_o(i,:))*ap_nnz(i), out[2] = sum ap_nnz(i)
+__global__ void k_outer_bounds(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *ap_nnz,
+                               unsigned long long *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long a = 0, b = 0, c = 0;
+  if (i < n) {
+    c = (unsigned long long)ap_nnz[i];
+    a = (unsigned long long)(pd_rp[i + 1] - pd_rp[i]) * c;
+    if (po_rp) b = (unsigned long long)(po_rp[i + 1] - po_rp[i]) * c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(FULL, a, o); b += __shfl_xor_sync(FULL, b, o); c += __shfl_xor_sync(FULL, c, o);
+  }
+  if (lane_id() == 0) {
+    if (a) atomicAdd(out, a);
+    if (b) atomicAdd(out + 1, b);
+    if (c) atomicAdd(out + 2, c);
+  }
+}
+
+// rehash the keys of an arena into a larger one (growth on overflow)
+__global__ void k_arena_rehash(Arena from, Arena to, int *status) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > from.mask) return;
+  unsigned long long k = from.keys[s];
+  if (k != EMPTY64) arena_insert(to.keys, to.mask, k, status);
+}
+
+// exact table sizes for the two-step P^T C~ rows: the length of the target
+// row of the allocated structure (C row, or staging row when present)
+__global__ void k_ptc_est(int64_t nrows, const int32_t *target_map, int64_t target_offset, int is_staging,
+                          int64_t t_nrows, const int32_t *t_rows, const int64_t *t_rp, int64_t *est) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrows) return;
+  int64_t tgt = target_map ? (int64_t)target_map[q] : q + target_offset;
+  int64_t r = tgt;
+  if (is_staging) {
+    r = lower_bound32(t_rows, 0, t_nrows, (int32_t)tgt);
+    if (r >= t_nrows || t_rows[r] != (int32_t)tgt) { est[q] = 0; return; }
+  }
+  est[q] = t_rp[r + 1] - t_rp[r];
+}
+
+// L2 flush: stream through a buffer larger than L2
+__global__ void k_touch(int4 *buf, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int4 v = buf[i];
+    v.x += 1;
+    buf[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// explicit instantiations via launch helpers
+// ---------------------------------------------------------------------------
+static int grid_for(unsigned long long groups, int groups_per_cta, int max_ctas) {
+  unsigned long long g = (groups + groups_per_cta - 1) / groups_per_cta;
+  if (g > (unsigned long long)max_ctas) g = max_ctas;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <typename K>
+static cudaError_t set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+#define PTAP_ROWKERNEL_DISPATCH(KERNEL, NUM, ...)                                                         \
+  do {                                                                                                     \
+    size_t gb = group_bytes(log2t, NUM);                                                                   \
+    if (group == 8) {                                                                                      \
+      int gpc = warps * 4;                                                                                 \
+      size_t sm = gtables ? 0 : gb * gpc;                                                                  \
+      if ((e = set_smem(KERNEL<8>, sm)) != cudaSuccess) return e;                                          \
+      int grid = gtables ? max_ctas : grid_for(nrows, gpc, max_ctas);                                      \
+      KERNEL<8><<<grid, warps * 32, sm, stream>>>(__VA_ARGS__);                                            \
+    } else {                                                                                               \
+      int gpc = warps;                                                                                     \
+      size_t sm = gtables ? 0 : gb * gpc;                                                                  \
+      if ((e = set_smem(KERNEL<32>, sm)) != cudaSuccess) return e;                                         \
+      int grid = gtables ? max_ctas : grid_for(nrows, gpc, max_ctas);                                      \
+      KERNEL<32><<<grid, warps * 32, sm, stream>>>(__VA_ARGS__);                                           \
+    }                                                                                                      \
+    return cudaGetLastError();                                                                             \
+  } while (0)
+
+cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                            int64_t *ap_nnz, int *status, cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_ap_count, false, op, rows, nrows, log2t, gtables, ap_nnz, status);
+}
+
+cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                  int do_send, int do_local, Arena local, Arena send, int *status,
+                                  cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_outer_symbolic, false, op, rows, nrows, log2t, gtables, do_send, do_local, local, send,
+                          status);
+}
+
+cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                 int do_send, int do_local, const OuterTargets &tg, int *status,
+                                 cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_outer_numeric, true, op, rows, nrows, log2t, gtables, do_send, do_local, tg, status);
+}
+
+cudaError_t launch_ct_fill(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                           const int64_t *ct_rp, int32_t *ct_col, int *status, cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_ct_fill, false, op, rows, nrows, log2t, gtables, ct_rp, ct_col, status);
+}
+
+cudaError_t launch_ct_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                              const int64_t *ct_rp, const int32_t *ct_col, double *ct_val, int *status,
+                              cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_ct_numeric, true, op, rows, nrows, log2t, gtables, ct_rp, ct_col, ct_val, status);
+}
+
+cudaError_t launch_ptc_numeric(const LaunchShape &s, const int32_t *rows, unsigned long long nrows,
+                               const int64_t *t_rp, const int32_t *t_row, const double *t_val,
+                               const int32_t *target_map, int64_t target_offset, const int64_t *ct_rp,
+                               const int32_t *ct_col, const double *ct_val, const PtcTarget &tg, int *status,
+                               cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_ptc_numeric, true, rows, nrows, log2t, gtables, t_rp, t_row, t_val, target_map,
+                          target_offset, ct_rp, ct_col, ct_val, tg, status);
+}
+
+size_t row_kernel_group_bytes(int log2t, bool num) { return group_bytes(log2t, num); }
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
+
+cudaError_t launch_row_work(const Ops &op, int64_t *apub, unsigned long long *mac, cudaStream_t st) {
+  if (op.nloc > 0) k_row_work<<<nblk(op.nloc, 256), 256, 0, st>>>(op, apub, mac);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_rp, const int64_t *po_rp, int mode,
+                            const BinLists &bl, unsigned long long *selected, cudaStream_t st) {
+  if (nrows > 0) k_bin_rows<<<nblk(nrows, 256), 256, 0, st>>>(nrows, est, pd_rp, po_rp, mode, bl, selected);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_est(const int32_t *rows, unsigned long long nrows, const int64_t *est, unsigned long long *mx,
+                           cudaStream_t st) {
+  if (nrows > 0) k_max_est<<<nblk((int64_t)nrows, 256), 256, 0, st>>>(rows, nrows, est, mx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_fill_empty(Arena ar, cudaStream_t st) {
+  unsigned long long cap = ar.mask + 1;
+  k_arena_fill_empty<<<nblk((int64_t)cap, 256), 256, 0, st>>>(ar.keys, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_insert_batch(Arena ar, int64_t nrows, const int32_t *rows, const int64_t *rp,
+                                      const int32_t *col, int64_t m, int64_t c_lo, int64_t c_hi, int *status,
+                                      cudaStream_t st) {
+  if (nrows > 0) k_arena_insert_batch<<<nblk(nrows * 32, 256), 256, 0, st>>>(ar, nrows, rows, rp, col, m, c_lo, c_hi, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_rowcount(Arena ar, int64_t m, int64_t *cnt, cudaStream_t st) {
+  unsigned long long cap = ar.mask + 1;
+  k_arena_rowcount<<<nblk((int64_t)cap, 256), 256, 0, st>>>(ar, (unsigned long long)m, cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_scatter(Arena ar, int64_t m, const int64_t *rp, int64_t *cursor, int32_t *col,
+                                 cudaStream_t st) {
+  unsigned long long cap = ar.mask + 1;
+  k_arena_scatter<<<nblk((int64_t)cap, 256), 256, 0, st>>>(ar, (unsigned long long)m, rp, cursor, col);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sort_rows(int64_t nrows, const int64_t *rp, int32_t *keys, int64_t *payload, int32_t *wide_rows,
+                             unsigned long long *nwide, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  const int warps = 8;
+  int grid = (int)((nrows + warps - 1) / warps);
+  if (grid > 148 * 16) grid = 148 * 16;
+  cudaError_t e;
+  if (payload) {
+    size_t sm = (size_t)warps * 1024 * 12;
+    if ((e = set_smem(k_sort_rows<true>, sm)) != cudaSuccess) return e;
+    k_sort_rows<true><<<grid, warps * 32, sm, st>>>(nrows, rp, keys, payload, wide_rows, nwide);
+  } else {
+    size_t sm = (size_t)warps * 1024 * 4;
+    k_sort_rows<false><<<grid, warps * 32, sm, st>>>(nrows, rp, keys, payload, wide_rows, nwide);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sort_rows_block(int64_t nwide, const int32_t *rows, const int64_t *rp, int32_t *keys,
+                                   int64_t *payload, int *status, cudaStream_t st) {
+  if (nwide <= 0) return cudaSuccess;
+  cudaError_t e;
+  size_t sm = 8192 * 4 + (payload ? 8192 * 8 : 0);
+  if (payload) {
+    if ((e = set_smem(k_sort_rows_block<true>, sm)) != cudaSuccess) return e;
+    k_sort_rows_block<true><<<(int)nwide, 1024, sm, st>>>(rows, rp, keys, payload, status);
+  } else {
+    if ((e = set_smem(k_sort_rows_block<false>, sm)) != cudaSuccess) return e;
+    k_sort_rows_block<false><<<(int)nwide, 1024, sm, st>>>(rows, rp, keys, payload, status);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_slots(int64_t nrows, const int32_t *rows, const int64_t *rp, const int32_t *col, int64_t c_lo,
+                               const int64_t *c_rp, const int32_t *c_col, int64_t *slot, int *status,
+                               cudaStream_t st) {
+  if (nrows > 0) k_merge_slots<<<nblk(nrows * 32, 256), 256, 0, st>>>(nrows, rows, rp, col, c_lo, c_rp, c_col, slot, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_add(int64_t n, const int64_t *slot, const double *vals, double *c_val, cudaStream_t st) {
+  if (n > 0) k_merge_add<<<nblk(n, 256), 256, 0, st>>>(n, slot, vals, c_val);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_cols(int64_t nnz, const int32_t *col, int64_t *cnt, cudaStream_t st) {
+  if (nnz > 0) k_count_cols<<<nblk(nnz, 256), 256, 0, st>>>(nnz, col, cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_scatter(int64_t nrows, const int64_t *rp, const int32_t *col, const int64_t *t_rp,
+                                     int64_t *cursor, int32_t *t_row, int64_t *t_perm, cudaStream_t st) {
+  if (nrows > 0) k_transpose_scatter<<<nblk(nrows, 256), 256, 0, st>>>(nrows, rp, col, t_rp, cursor, t_row, t_perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(int64_t n, const int64_t *perm, const double *src, double *dst, cudaStream_t st) {
+  if (n > 0) k_gather<<<nblk(n, 256), 256, 0, st>>>(n, perm, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ptc_symbolic(int64_t nrows, const int64_t *t_rp, const int32_t *t_row, const int32_t *target_map,
+                                int64_t target_offset, const int64_t *ct_rp, const int32_t *ct_col, Arena ar,
+                                int64_t m, int *status, cudaStream_t st) {
+  if (nrows > 0)
+    k_ptc_symbolic<<<nblk(nrows * 32, 256), 256, 0, st>>>(nrows, t_rp, t_row, target_map, target_offset, ct_rp,
+                                                          ct_col, ar, (unsigned long long)m, status);
+  return cudaGetLastError();
+}
+
+cudaError_t scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *scratch, cudaStream_t st) {
+  // out has n+1 entries; scratch must hold scan_scratch_elems(n) int64
+  if (n <= 0) {
+    cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+    return cudaGetLastError();
+  }
+  int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  int64_t *tile_sums = scratch;
+  int64_t *tile_off = scratch + tiles;
+  k_scan_tiles<<<(int)tiles, SCAN_THREADS, 0, st>>>(in, out, n, tile_sums);
+  if (tiles > 1) {
+    cudaError_t e = scan_exclusive(tile_sums, tile_off, tiles, scratch + 2 * tiles + 1, st);
+    if (e != cudaSuccess) return e;
+    k_scan_add<<<nblk(n, 256), 256, 0, st>>>(out, n, tile_off);
+  }
+  k_set_total<<<1, 1, 0, st>>>(out, n, in);
+  return cudaGetLastError();
+}
+
+int64_t scan_scratch_elems(int64_t n) {
+  int64_t tot = 0;
+  while (n > 1) {
+    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    tot += 2 * tiles + 1;
+    n = tiles;
+  }
+  return tot + 4;
+}
+
+cudaError_t launch_nonzero_flags(int64_t n, const int64_t *cnt, int64_t *flags, cudaStream_t st) {
+  if (n > 0) k_nonzero_flags<<<nblk(n, 256), 256, 0, st>>>(n, cnt, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_rows(int64_t n, const int64_t *cnt, const int64_t *pos, const int64_t *dense_rp,
+                                int32_t *rows, int64_t *rp, cudaStream_t st) {
+  if (n > 0) k_compact_rows<<<nblk(n, 256), 256, 0, st>>>(n, cnt, pos, dense_rp, rows, rp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iota32(int32_t *p, int64_t n, cudaStream_t st) {
+  if (n > 0) k_iota32<<<nblk(n, 256), 256, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_lengths(int64_t n, const int64_t *rp, int64_t *len, cudaStream_t st) {
+  if (n > 0) k_row_lengths<<<nblk(n, 256), 256, 0, st>>>(n, rp, len);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_outer_bounds(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *ap_nnz,
+                                unsigned long long *out, cudaStream_t st) {
+  if (n > 0) k_outer_bounds<<<nblk(n, 256), 256, 0, st>>>(n, pd_rp, po_rp, ap_nnz, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_rehash(Arena from, Arena to, int *status, cudaStream_t st) {
+  unsigned long long cap = from.mask + 1;
+  k_arena_rehash<<<nblk((int64_t)cap, 256), 256, 0, st>>>(from, to, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t target_offset, int is_staging,
+                           int64_t t_nrows, const int32_t *t_rows, const int64_t *t_rp, int64_t *est,
+                           cudaStream_t st) {
+  if (nrows > 0)
+    k_ptc_est<<<nblk(nrows, 256), 256, 0, st>>>(nrows, target_map, target_offset, is_staging, t_nrows, t_rows, t_rp, est);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_touch(void *buf, int64_t bytes, cudaStream_t st) {
+  int64_t n = bytes / 16;
+  k_touch<<<148 * 8, 256, 0, st>>>((int4 *)buf, n);
+  return cudaGetLastError();
+}
+
+}  // namespace ptapdev

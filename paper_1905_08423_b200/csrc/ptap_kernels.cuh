@@ -1,0 +1,112 @@
+// ptap_kernels.cuh -- host-callable launchers of the kernels in ptap_kernels.cu
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ptap_device.cuh"
+
+namespace ptapdev {
+
+// Work bins: estimated distinct AP-row keys n -> table shape.
+//   bin 0: n <= 32    4 rows per warp (8-lane groups), 64-slot shared tables
+//   bin 1: n <= 256   1 row per warp, 512-slot shared tables
+//   bin 2: n <= 2048  1 row per warp, 4096-slot shared tables
+//   bin 3: larger     1 row per warp, global-memory tables (heavy rows)
+constexpr int NBINS = 4;
+__host__ __device__ inline int64_t bin_capacity(int q) { return q == 0 ? 32 : (q == 1 ? 256 : 2048); }
+
+struct BinLists {
+  int32_t *rows[NBINS];
+  unsigned long long *count;  // device, NBINS entries
+};
+
+struct Arena {
+  unsigned long long *keys;
+  unsigned long long mask;  // capacity - 1 (power of two)
+};
+
+struct OuterTargets {
+  const int64_t *c_rp; const int32_t *c_col; double *c_val;     // local C rows (global columns)
+  int64_t s_nrows; const int32_t *s_rows; const int64_t *s_rp; const int32_t *s_col; double *s_val;  // staging
+};
+
+struct PtcTarget {
+  int is_staging;
+  int64_t nrows;
+  const int32_t *rows;  // staging row ids (global), for lookup
+  const int64_t *rp;
+  const int32_t *col;
+  double *val;
+};
+
+struct LaunchShape {
+  int group;     // 8 or 32 lanes per row
+  int warps;     // warps per CTA
+  int log2t;     // table slots = 1 << log2t
+  int max_ctas;  // grid cap (grid-stride loops)
+  unsigned char *gtables;  // non-null: tables in global memory (one per group of the capped grid)
+};
+
+size_t row_kernel_group_bytes(int log2t, bool num);
+
+cudaError_t launch_row_work(const Ops &op, int64_t *apub, unsigned long long *mac, cudaStream_t st);
+cudaError_t launch_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_rp, const int64_t *po_rp, int mode,
+                            const BinLists &bl, unsigned long long *selected, cudaStream_t st);
+cudaError_t launch_max_est(const int32_t *rows, unsigned long long nrows, const int64_t *est, unsigned long long *mx,
+                           cudaStream_t st);
+cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                            int64_t *ap_nnz, int *status, cudaStream_t stream);
+cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                  int do_send, int do_local, Arena local, Arena send, int *status,
+                                  cudaStream_t stream);
+cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                 int do_send, int do_local, const OuterTargets &tg, int *status,
+                                 cudaStream_t stream);
+cudaError_t launch_ct_fill(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                           const int64_t *ct_rp, int32_t *ct_col, int *status, cudaStream_t stream);
+cudaError_t launch_ct_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                              const int64_t *ct_rp, const int32_t *ct_col, double *ct_val, int *status,
+                              cudaStream_t stream);
+cudaError_t launch_ptc_numeric(const LaunchShape &s, const int32_t *rows, unsigned long long nrows,
+                               const int64_t *t_rp, const int32_t *t_row, const double *t_val,
+                               const int32_t *target_map, int64_t target_offset, const int64_t *ct_rp,
+                               const int32_t *ct_col, const double *ct_val, const PtcTarget &tg, int *status,
+                               cudaStream_t stream);
+cudaError_t launch_arena_fill_empty(Arena ar, cudaStream_t st);
+cudaError_t launch_arena_insert_batch(Arena ar, int64_t nrows, const int32_t *rows, const int64_t *rp,
+                                      const int32_t *col, int64_t m, int64_t c_lo, int64_t c_hi, int *status,
+                                      cudaStream_t st);
+cudaError_t launch_arena_rowcount(Arena ar, int64_t m, int64_t *cnt, cudaStream_t st);
+cudaError_t launch_arena_scatter(Arena ar, int64_t m, const int64_t *rp, int64_t *cursor, int32_t *col,
+                                 cudaStream_t st);
+cudaError_t launch_sort_rows(int64_t nrows, const int64_t *rp, int32_t *keys, int64_t *payload, int32_t *wide_rows,
+                             unsigned long long *nwide, cudaStream_t st);
+cudaError_t launch_sort_rows_block(int64_t nwide, const int32_t *rows, const int64_t *rp, int32_t *keys,
+                                   int64_t *payload, int *status, cudaStream_t st);
+cudaError_t launch_merge_slots(int64_t nrows, const int32_t *rows, const int64_t *rp, const int32_t *col, int64_t c_lo,
+                               const int64_t *c_rp, const int32_t *c_col, int64_t *slot, int *status,
+                               cudaStream_t st);
+cudaError_t launch_merge_add(int64_t n, const int64_t *slot, const double *vals, double *c_val, cudaStream_t st);
+cudaError_t launch_count_cols(int64_t nnz, const int32_t *col, int64_t *cnt, cudaStream_t st);
+cudaError_t launch_transpose_scatter(int64_t nrows, const int64_t *rp, const int32_t *col, const int64_t *t_rp,
+                                     int64_t *cursor, int32_t *t_row, int64_t *t_perm, cudaStream_t st);
+cudaError_t launch_gather(int64_t n, const int64_t *perm, const double *src, double *dst, cudaStream_t st);
+cudaError_t launch_ptc_symbolic(int64_t nrows, const int64_t *t_rp, const int32_t *t_row, const int32_t *target_map,
+                                int64_t target_offset, const int64_t *ct_rp, const int32_t *ct_col, Arena ar,
+                                int64_t m, int *status, cudaStream_t st);
+cudaError_t scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *scratch, cudaStream_t st);
+int64_t scan_scratch_elems(int64_t n);
+cudaError_t launch_nonzero_flags(int64_t n, const int64_t *cnt, int64_t *flags, cudaStream_t st);
+cudaError_t launch_compact_rows(int64_t n, const int64_t *cnt, const int64_t *pos, const int64_t *dense_rp,
+                                int32_t *rows, int64_t *rp, cudaStream_t st);
+cudaError_t launch_iota32(int32_t *p, int64_t n, cudaStream_t st);
+cudaError_t launch_row_lengths(int64_t n, const int64_t *rp, int64_t *len, cudaStream_t st);
+cudaError_t launch_outer_bounds(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *ap_nnz,
+                                unsigned long long *out, cudaStream_t st);
+cudaError_t launch_arena_rehash(Arena from, Arena to, int *status, cudaStream_t st);
+cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t target_offset, int is_staging,
+                           int64_t t_nrows, const int32_t *t_rows, const int64_t *t_rp, int64_t *est,
+                           cudaStream_t st);
+cudaError_t launch_touch(void *buf, int64_t bytes, cudaStream_t st);
+
+}  // namespace ptapdev

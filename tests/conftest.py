@@ -61,3 +61,31 @@ def row_scaled_err(ip, got, want):
     np.maximum.at(rmax, rows, np.abs(want))
     den = np.maximum(rmax[rows], 1e-300)
     return float((np.abs(got - want) / den).max(initial=0.0))
+
+
+def csr_from_arrays(nrows, ncols, ip, j, v):
+    from paper_1905_08423_b200 import CsrMatrix
+    return CsrMatrix(nrows, ncols, ip, j, v, check=False)
+
+
+def run_ptap(a_glob, p_glob, nranks, algorithm, cache="keep"):
+    """Distribute, one symbolic + one numeric pass on the CUDA path, assemble C
+    (the reference's tests/conftest.py:48-58 helper, on this package)."""
+    import paper_1905_08423_b200 as pk
+
+    def prog(ctx):
+        a, p = pk.distribute(a_glob, p_glob, ctx.nranks, ctx.rank)
+        c, plan = pk.ptap(a, p, algorithm, ctx, cache=cache)
+        return c.local, plan.counters, ctx.ledger.snapshot()
+
+    results = pk.spawn_ranks(nranks, prog)
+    c = pk.assemble_global([r[0] for r in results], ncols=p_glob.ncols)
+    return c, results
+
+
+def gpu_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
