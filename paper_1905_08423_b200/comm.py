@@ -283,6 +283,10 @@ def exchange_values(ctx: RankContext, staging_val, route: ContributionRoute, asy
 
 
 def _rank_main(rank, nranks, port, program, queue, backend):
+    if isinstance(program, bytes):
+        import cloudpickle
+
+        program = cloudpickle.loads(program)
     torch = _torch()
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(nranks),
                       LOCAL_RANK="0")
@@ -317,9 +321,19 @@ def spawn_ranks(nranks: int, program, *, backend: str = "gloo", timeout: float =
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mpctx = mp.get_context("fork")
+    torch = _torch()
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        # CUDA cannot be re-initialised in a forked child: spawn, shipping the
+        # program (usually a closure) by value
+        import cloudpickle
+
+        mpctx = mp.get_context("spawn")
+        payload = cloudpickle.dumps(program)
+    else:
+        mpctx = mp.get_context("fork")
+        payload = program
     q = mpctx.Queue()
-    procs = [mpctx.Process(target=_rank_main, args=(r, nranks, port, program, q, backend)) for r in range(nranks)]
+    procs = [mpctx.Process(target=_rank_main, args=(r, nranks, port, payload, q, backend)) for r in range(nranks)]
     for p in procs:
         p.start()
     results = [None] * nranks

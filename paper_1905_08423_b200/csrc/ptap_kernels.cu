@@ -553,6 +553,8 @@ __global__ void __launch_bounds__(256) k_ptc_numeric(const int32_t *rows, unsign
     }
     if (!ok) atomicOr(status, ST_TABLE_FULL);
     nnew = group_sum<GROUP>(nnew);
+    int found = 0;
+    bool checked = false;
     if (q >= 0) {
       int64_t tgt = target_map ? (int64_t)target_map[q] : q + target_offset;
       int64_t r = tgt;
@@ -563,8 +565,8 @@ __global__ void __launch_bounds__(256) k_ptc_numeric(const int32_t *rows, unsign
       if (r < 0) {
         if (nnew > 0 && gl == 0) atomicOr(status, ST_DRIFT);
       } else {
+        checked = true;
         int64_t c0 = tg.rp[r], c1 = tg.rp[r + 1];
-        int found = 0;
         for (int64_t e = c0 + gl; e < c1; e += GROUP) {
           int s = table_find(tb.keys, log2t, tg.col[e]);
           if (s >= 0) {
@@ -575,10 +577,10 @@ __global__ void __launch_bounds__(256) k_ptc_numeric(const int32_t *rows, unsign
             if (tg.is_staging) atomicOr(status, ST_DRIFT);
           }
         }
-        found = group_sum<GROUP>(found);
-        if (found != nnew && gl == 0) atomicOr(status, ST_DRIFT);
       }
     }
+    found = group_sum<GROUP>(found);  // warp-collective: outside the per-group branches
+    if (checked && found != nnew && gl == 0) atomicOr(status, ST_DRIFT);
     __syncwarp();
   }
 }
