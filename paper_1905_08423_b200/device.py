@@ -60,9 +60,12 @@ class DeviceCsr:
                    torch.zeros(0, dtype=torch.int32, device=device),
                    torch.zeros(0, dtype=torch.float64, device=device))
 
-    def set_values(self, values: np.ndarray, non_blocking=False):
+    def set_values(self, values, non_blocking=False):
         torch = _torch()
-        src = torch.from_numpy(np.ascontiguousarray(values, np.float64))
+        if isinstance(values, torch.Tensor):
+            src = values
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(values, np.float64))
         if self.val is None or self.val.numel() != src.numel():
             self.val = src.to(self.row_ptr.device, non_blocking=non_blocking)
         else:

@@ -222,8 +222,16 @@ class TripleProductPlan:
         """Copy the current C values to the host LocalMatrix view."""
         alloc = self.c_alloc
         _, _, val_d = self.c_device()
-        vals = val_d.cpu().numpy()
         diag_idx, off_idx = self._c_host
+        if off_idx.size == 0:
+            # every column owned: C values are the diag values in order
+            if getattr(self, "_pinned_c", None) is None or self._pinned_c.numel() != val_d.numel():
+                self._pinned_c = _torch().empty(val_d.numel(), dtype=_torch().float64,
+                                                pin_memory=_torch().cuda.is_available())
+            self._pinned_c.copy_(val_d)
+            alloc.local.diag.values = self._pinned_c.numpy()
+            return alloc.local
+        vals = val_d.cpu().numpy()
         alloc.local.diag.values[:] = vals[diag_idx]
         alloc.local.offdiag.values[:] = vals[off_idx]
         return alloc.local
@@ -282,13 +290,14 @@ def _prepare(plan: TripleProductPlan, a: DistMatrix, p: DistMatrix, ctx: RankCon
         plan._a_dev = _device_local(a, dev)
         plan._p_dev = _device_local(p, dev)
         if isinstance(a.local, LocalMatrix):
-            plan._a_token = structure_token(a.local)
+            plan._a_token = (_identity(a.local), structure_token(a.local))
         if isinstance(p.local, LocalMatrix):
-            plan._p_token = structure_token(p.local)
+            plan._p_token = (_identity(p.local), structure_token(p.local))
         return
     for which, m, tok in (("A", a, plan._a_token), ("P", p, plan._p_token)):
         if isinstance(m.local, LocalMatrix):
-            if tok is not None and structure_token(m.local) != tok:
+            # same (frozen) structure arrays as at symbolic time: no hashing needed
+            if tok is not None and _identity(m.local) != tok[0] and structure_token(m.local) != tok[1]:
                 raise StructuralDriftError(f"{which} changed structure since the symbolic phase")
             target = plan._a_dev if which == "A" else plan._p_dev
             target.refresh_values(m.local)
@@ -300,6 +309,11 @@ def _prepare(plan: TripleProductPlan, a: DistMatrix, p: DistMatrix, ctx: RankCon
                 else:
                     plan._p_dev = m.local
     plan._ops.a, plan._ops.p = plan._a_dev, plan._p_dev
+
+
+def _identity(lm: LocalMatrix) -> tuple:
+    return tuple(id(x) for x in (lm.diag.row_offsets, lm.diag.col_indices, lm.offdiag.row_offsets,
+                                 lm.offdiag.col_indices, lm.col_map))
 
 
 def _remote_csr(rr: RemoteRows, m: int, device) -> DeviceCsr:
