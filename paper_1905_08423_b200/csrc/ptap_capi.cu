@@ -264,7 +264,7 @@ ptap_status build_bins(ptap_plan *p, BinSet &bs, int64_t nrows, const int64_t *e
     CK(cudaStreamSynchronize(st));
     bs.log2t_global = ceil_log2(2 * (mx > 0 ? mx : 1));
     LaunchShape s = shape_for(NBINS - 1, bs);
-    size_t bytes = (size_t)s.max_ctas * s.warps * row_kernel_group_bytes(bs.log2t_global, num);
+    size_t bytes = (size_t)s.max_ctas * s.warps * row_kernel_group_bytes(bs.log2t_global, num, s.group);
     CKS(palloc(p, &bs.gtables, (int64_t)bytes, cat, st));
   }
   return PTAP_OK;

@@ -102,16 +102,56 @@ __device__ __forceinline__ int table_find(const int32_t *keys, int log2t, int32_
   return -1;
 }
 
-// Row i of A*P accumulated by one lane group of GROUP lanes, in the
-// reference's fold order (src/_kernels.py:205-227): the A_d entries of row i
-// in ascending order, then the A_o entries; for every A entry the whole P
-// row is scattered in one step (its columns are distinct, so the step is
-// conflict-free).  i < 0 marks an idle group (it still joins the shuffles).
-// Returns (per lane) the number of new keys this lane inserted.
+// Pairs (A entry, P entry) of one batch of A entries, flattened in the
+// reference's fold order and staged in shared memory per lane group.
+constexpr int PAIRS_PER_LANE = 8;  // window = PAIRS_PER_LANE * GROUP pairs
+
+struct PStage {
+  int32_t *desc;  // [window] P entry index; bit 31 set = P_o entry
+  double *a;      // [window] the A value of the pair (numeric only)
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+
+// Find g in the table or claim an empty slot for it; returns the slot and
+// sets `existed`.  Only keys distinct within the calling lanes may race.
+__device__ __forceinline__ int table_find_or_claim(int32_t *keys, int log2t, int32_t g, bool &existed) {
+  const uint32_t mask = (1u << log2t) - 1u;
+  uint32_t h = hash32((uint32_t)g, log2t);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    int32_t k = keys[h];
+    if (k == g) { existed = true; return (int)h; }
+    if (k == EMPTY32) {
+      int32_t old = atomicCAS(keys + h, EMPTY32, g);
+      if (old == EMPTY32) { existed = false; return (int)h; }
+      if (old == g) { existed = true; return (int)h; }
+    }
+    h = (h + 1) & mask;
+  }
+  existed = false;
+  return -1;
+}
+
+// Row i of A*P accumulated by one lane group of GROUP lanes.  Fold order is
+// the reference's (src/_kernels.py:205-227): A_d entries ascending, then A_o
+// entries; for a key g the products are added left to right in that order,
+// the first product setting the slot (hm_add semantics, :116-147).
+//
+// The (A entry, P entry) pairs of a batch of GROUP A entries are flattened
+// (GROUP lanes each take a pair per round, so P rows are read coalesced and
+// every lane is busy), then the lanes of a round that carry the same key are
+// grouped with __match_any_sync: the lowest such lane folds the others' products
+// into the table value in lane (= pair) order.  Distinct rows of a warp use
+// distinct tables, so the match key carries the group id.
+// i < 0 marks an idle group (it still joins every warp-collective).  Returns
+// (per lane) the number of new keys this lane created.
 template <int GROUP, bool NUM>
 __device__ __forceinline__ int ap_row_accumulate(const Ops &op, int64_t i, int32_t *keys, double *vals,
-                                                 int log2t, int *status) {
-  const int gl = threadIdx.x & (GROUP - 1);
+                                                 int log2t, const PStage &ps, int *status) {
+  const int lane = lane_id();
+  const int gl = lane & (GROUP - 1);
+  const unsigned gid = (unsigned)(lane / GROUP);
+  const int WIN = PAIRS_PER_LANE * GROUP;
   int nnew = 0;
   bool ok = true;
 #pragma unroll 1
@@ -120,49 +160,94 @@ __device__ __forceinline__ int ap_row_accumulate(const Ops &op, int64_t i, int32
     if (arp == nullptr) continue;  // uniform
     const int32_t *acol = src ? op.ao_col : op.ad_col;
     const double *aval = src ? op.ao_val : op.ad_val;
+    const int32_t *qcol = src ? op.pr_col : op.pd_col;
+    const double *qval = src ? op.pr_val : op.pd_val;
+    const int32_t coff = src ? 0 : (int32_t)op.c_lo;
     int64_t t0 = 0, t1 = 0;
     if (i >= 0) { t0 = __ldg(arp + i); t1 = __ldg(arp + i + 1); }
     int len = (int)(t1 - t0);
     int maxlen = __reduce_max_sync(FULL, len);
 #pragma unroll 1
     for (int tb = 0; tb < maxlen; tb += GROUP) {
-      // each lane of the group preloads one A entry and its P row bounds
+      // each lane owns one A entry of the batch: its value and P row bounds
       int t = tb + gl;
       double a = 0.0;
-      int64_t d0 = 0, d1 = 0, o0 = 0, o1 = 0;
+      int64_t d0 = 0, o0 = 0;
+      int nd = 0, plen = 0;
       if (t < len) {
         int32_t k = __ldg(acol + t0 + t);
         if (NUM) a = __ldg(aval + t0 + t);
         if (src == 0) {
-          d0 = __ldg(op.pd_rp + k); d1 = __ldg(op.pd_rp + k + 1);
-          if (op.po_rp) { o0 = __ldg(op.po_rp + k); o1 = __ldg(op.po_rp + k + 1); }
+          d0 = __ldg(op.pd_rp + k);
+          nd = (int)(__ldg(op.pd_rp + k + 1) - d0);
+          if (op.po_rp) { o0 = __ldg(op.po_rp + k); plen = nd + (int)(__ldg(op.po_rp + k + 1) - o0); }
+          else plen = nd;
         } else {
-          d0 = __ldg(op.pr_rp + k); d1 = __ldg(op.pr_rp + k + 1);
+          d0 = __ldg(op.pr_rp + k);
+          nd = plen = (int)(__ldg(op.pr_rp + k + 1) - d0);
         }
       }
-      int steps = min(GROUP, maxlen - tb);
+      // exclusive scan of the pair counts inside the group
+      int incl = plen;
+#pragma unroll
+      for (int o = 1; o < GROUP; o <<= 1) {
+        int y = __shfl_up_sync(FULL, incl, o, GROUP);
+        if (gl >= o) incl += y;
+      }
+      int excl = incl - plen;
+      int total = __shfl_sync(FULL, incl, GROUP - 1, GROUP);
+      int maxtotal = __reduce_max_sync(FULL, total);
 #pragma unroll 1
-      for (int j = 0; j < steps; ++j) {
-        double aj = __shfl_sync(FULL, a, j, GROUP);
-        int64_t sd0 = __shfl_sync(FULL, d0, j, GROUP), sd1 = __shfl_sync(FULL, d1, j, GROUP);
-        int64_t so0 = __shfl_sync(FULL, o0, j, GROUP), so1 = __shfl_sync(FULL, o1, j, GROUP);
-        int nd = (int)(sd1 - sd0);
-        int plen = nd + (int)(so1 - so0);
-        if (tb + j >= len) plen = 0;
-        for (int u = gl; u < plen; u += GROUP) {
-          int32_t g;
-          double p = 0.0;
-          if (u < nd) {
-            if (src == 0) { g = __ldg(op.pd_col + sd0 + u) + (int32_t)op.c_lo; if (NUM) p = __ldg(op.pd_val + sd0 + u); }
-            else { g = __ldg(op.pr_col + sd0 + u); if (NUM) p = __ldg(op.pr_val + sd0 + u); }
-          } else {
-            int64_t e = so0 + (u - nd);
-            g = __ldg(op.p_colmap + __ldg(op.po_col + e));
-            if (NUM) p = __ldg(op.po_val + e);
-          }
-          ok &= table_put<NUM>(keys, vals, log2t, g, NUM ? __dmul_rn(aj, p) : 0.0, nnew);
+      for (int w0 = 0; w0 < maxtotal; w0 += WIN) {
+        // expansion: lane writes the descriptors of its pairs inside the window
+        int ub = max(0, w0 - excl), ue = min(plen, w0 + WIN - excl);
+        for (int u = ub; u < ue; ++u) {
+          int q = excl + u - w0;
+          ps.desc[q] = u < nd ? (int32_t)(d0 + u) : (int32_t)((uint32_t)(o0 + (u - nd)) | 0x80000000u);
+          if (NUM) ps.a[q] = a;
         }
         __syncwarp();
+        int wtot = min(total - w0, WIN);
+        int rounds = (__reduce_max_sync(FULL, max(wtot, 0)) + GROUP - 1) / GROUP;
+#pragma unroll 1
+        for (int r = 0; r < rounds; ++r) {
+          int q = r * GROUP + gl;
+          bool valid = i >= 0 && q < wtot;
+          int32_t g = 0;
+          double v = 0.0;
+          if (valid) {
+            int32_t e = ps.desc[q];
+            double pv = 0.0;
+            if (e >= 0) { g = __ldg(qcol + e) + coff; if (NUM) pv = __ldg(qval + e); }
+            else {
+              int32_t eo = e & 0x7fffffff;
+              g = __ldg(op.p_colmap + __ldg(op.po_col + eo));
+              if (NUM) pv = __ldg(op.po_val + eo);
+            }
+            if (NUM) v = __dmul_rn(ps.a[q], pv);
+          }
+          unsigned long long key = valid ? (((unsigned long long)gid << 32) | (uint32_t)g)
+                                         : (0xFFFFFFFF00000000ull | (unsigned)lane);
+          unsigned grp = __match_any_sync(FULL, key);
+          bool leader = valid && (__ffs(grp) - 1) == lane;
+          unsigned rest = grp & ~(1u << lane);
+          bool existed = false;
+          int slot = leader ? table_find_or_claim(keys, log2t, g, existed) : 0;
+          if (leader && slot < 0) ok = false;
+          double acc = 0.0;
+          if (NUM && leader && slot >= 0) acc = existed ? __dadd_rn(vals[slot], v) : v;
+          if (NUM) {
+            int steps = __reduce_max_sync(FULL, leader ? __popc(rest) : 0);
+            for (int it = 0; it < steps; ++it) {
+              int srcl = (leader && rest) ? __ffs(rest) - 1 : lane;
+              double x = __shfl_sync(FULL, v, srcl);
+              if (leader && rest) { acc = __dadd_rn(acc, x); rest &= rest - 1; }
+            }
+            if (leader && slot >= 0) vals[slot] = acc;
+          }
+          if (leader && slot >= 0 && !existed) ++nnew;
+          __syncwarp();
+        }
       }
     }
   }

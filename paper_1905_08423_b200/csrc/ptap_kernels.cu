@@ -91,40 +91,49 @@ __global__ void k_max_est(const int32_t *rows, unsigned long long nrows, const i
 // group-table addressing shared by the row kernels
 // ---------------------------------------------------------------------------
 struct GroupTables {
-  int32_t *keys; double *vals; int32_t *lk; double *lv;
+  int32_t *keys; double *vals; int32_t *lk;
+  PStage ps;
 };
-// per-group footprint: vals[T] lv[T/2] (fp64) then keys[T] lk[T/2] (int32)
-__host__ __device__ inline size_t group_bytes(int log2t, bool num) {
+// per-group footprint: 8-byte items first (vals[T], a[WIN]) then 4-byte
+// items (keys[T], lk[T/2], desc[WIN]); WIN = PAIRS_PER_LANE * GROUP
+__host__ __device__ inline size_t group_bytes(int log2t, bool num, int group) {
   size_t T = (size_t)1 << log2t;
-  return num ? (T * 8 + (T / 2) * 8 + T * 4 + (T / 2) * 4) : (T * 4 + (T / 2) * 4);
+  size_t W = (size_t)PAIRS_PER_LANE * group;
+  size_t b8 = num ? (T + W) * 8 : 0;
+  size_t b4 = T * 4 + (T / 2) * 4 + W * 4;
+  return (b8 + b4 + 15) & ~(size_t)15;
 }
-template <int GROUP, bool NUM>
+template <int GROUP, bool NUM, bool GT>
 __device__ __forceinline__ GroupTables group_tables(unsigned char *gtables, int log2t) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int gpw = 32 / GROUP;
   const int gid = (threadIdx.x >> 5) * gpw + lane_id() / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
-  size_t gb = group_bytes(log2t, NUM);
-  unsigned char *base = gtables ? gtables + ((size_t)blockIdx.x * gpc + gid) * gb : smem + (size_t)gid * gb;
+  size_t gb = group_bytes(log2t, NUM, GROUP);
+  unsigned char *base = GT ? gtables + ((size_t)blockIdx.x * gpc + gid) * gb : smem + (size_t)gid * gb;
   const int T = 1 << log2t;
+  const int W = PAIRS_PER_LANE * GROUP;
   GroupTables t;
+  unsigned char *q = base;
   if (NUM) {
-    t.vals = (double *)base; t.lv = t.vals + T;
-    t.keys = (int32_t *)(t.lv + T / 2); t.lk = t.keys + T;
+    t.vals = (double *)q; q += (size_t)T * 8;
+    t.ps.a = (double *)q; q += (size_t)W * 8;
   } else {
-    t.vals = nullptr; t.lv = nullptr;
-    t.keys = (int32_t *)base; t.lk = t.keys + T;
+    t.vals = nullptr; t.ps.a = nullptr;
   }
+  t.keys = (int32_t *)q; q += (size_t)T * 4;
+  t.lk = (int32_t *)q; q += (size_t)(T / 2) * 4;
+  t.ps.desc = (int32_t *)q;
   return t;
 }
 
 // ---------------------------------------------------------------------------
 // exact AP row sizes
 // ---------------------------------------------------------------------------
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_ap_count(Ops op, const int32_t *rows, unsigned long long nrows, int log2t,
                                                   unsigned char *gtables, int64_t *ap_nnz, int *status) {
-  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, false, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(256) k_ap_count(Ops op, const int32_t *rows, u
     unsigned long long ridx = r0 + lane_id() / GROUP;
     int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
     table_clear<GROUP>(tb.keys, T);
-    int nnew = ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    int nnew = ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, tb.ps, status);
     nnew = group_sum<GROUP>(nnew);
     if (i >= 0 && (lane_id() & (GROUP - 1)) == 0) ap_nnz[i] = nnew;
     __syncwarp();
@@ -161,11 +170,11 @@ __device__ __forceinline__ void arena_insert(unsigned long long *ar, unsigned lo
 // structural outer products P(i,:) (x) AP(i,:) (src/_kernels.py:361-418):
 // local rows go to the local arena keyed (J - c_lo)*m + g, send rows to the
 // send arena keyed J*m + g.
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *rows, unsigned long long nrows,
                                                         int log2t, unsigned char *gtables, int do_send,
                                                         int do_local, Arena local, Arena send, int *status) {
-  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, false, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
     bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
     if (!(wl || ws)) i = -1;
     table_clear<GROUP>(tb.keys, T);
-    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, tb.ps, status);
     int n = table_compact<GROUP, false>(tb.keys, nullptr, T, tb.lk, nullptr);
     if (i >= 0 && n > 0) {
       if (wl) {
@@ -333,11 +342,11 @@ __global__ void __launch_bounds__(1024) k_sort_rows_block(const int32_t *rows, c
 // ---------------------------------------------------------------------------
 // fused numeric all-at-once / merged (src/_kernels.py:446-515)
 // ---------------------------------------------------------------------------
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_outer_numeric(Ops op, const int32_t *rows, unsigned long long nrows,
                                                        int log2t, unsigned char *gtables, int do_send,
                                                        int do_local, OuterTargets tg, int *status) {
-  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, true, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -355,37 +364,46 @@ __global__ void __launch_bounds__(256) k_outer_numeric(Ops op, const int32_t *ro
     if (!(wl || ws)) i = -1;
     if (__all_sync(FULL, i < 0)) continue;
     table_clear<GROUP>(tb.keys, T);
-    ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, status);
-    int n = table_compact<GROUP, true>(tb.keys, tb.vals, T, tb.lk, tb.lv);
-    if (i >= 0 && n > 0) {
-      if (wl) {
-        int tot = (int)(pd1 - pd0) * n;
-        for (int f = gl; f < tot; f += GROUP) {
-          int jj = f / n, e = f - jj * n;
+    int n = group_sum<GROUP>(ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, tb.ps, status));
+    // outer product P(i,:) (x) AP(i,:): for each target row J, the lanes walk
+    // C's stored row J (coalesced columns) and pull the matching AP value
+    // from the group's table; every AP key must be found in every row J.
+    int nj_l = wl ? (int)(pd1 - pd0) : 0;
+    int nj_s = ws ? (int)(po1 - po0) : 0;
+    int maxj = __reduce_max_sync(FULL, nj_l + nj_s);
+    for (int jj = 0; jj < maxj; ++jj) {
+      int found = 0;
+      bool live = i >= 0 && jj < nj_l + nj_s;
+      if (live) {
+        int64_t c0, c1;
+        double pij;
+        const int32_t *ccol;
+        double *cval;
+        bool row_ok = true;
+        if (jj < nj_l) {
           int32_t J = __ldg(op.pd_col + pd0 + jj);
-          double pij = __ldg(op.pd_val + pd0 + jj);
-          int32_t g = tb.lk[e];
-          int64_t c0 = __ldg(tg.c_rp + J), c1 = __ldg(tg.c_rp + J + 1);
-          int64_t pos = lower_bound32(tg.c_col, c0, c1, g);
-          if (pos < c1 && __ldg(tg.c_col + pos) == g) atomicAdd(tg.c_val + pos, __dmul_rn(pij, tb.lv[e]));
-          else atomicOr(status, ST_DRIFT);
-        }
-      }
-      if (ws) {
-        int tot = (int)(po1 - po0) * n;
-        for (int f = gl; f < tot; f += GROUP) {
-          int jj = f / n, e = f - jj * n;
-          int32_t Jg = __ldg(op.p_colmap + __ldg(op.po_col + po0 + jj));
-          double pij = __ldg(op.po_val + po0 + jj);
-          int32_t g = tb.lk[e];
+          pij = __ldg(op.pd_val + pd0 + jj);
+          c0 = __ldg(tg.c_rp + J); c1 = __ldg(tg.c_rp + J + 1);
+          ccol = tg.c_col; cval = tg.c_val;
+        } else {
+          int64_t e = po0 + (jj - nj_l);
+          int32_t Jg = __ldg(op.p_colmap + __ldg(op.po_col + e));
+          pij = __ldg(op.po_val + e);
           int64_t sr = lower_bound32(tg.s_rows, 0, tg.s_nrows, Jg);
-          if (sr >= tg.s_nrows || __ldg(tg.s_rows + sr) != Jg) { atomicOr(status, ST_DRIFT); continue; }
-          int64_t c0 = __ldg(tg.s_rp + sr), c1 = __ldg(tg.s_rp + sr + 1);
-          int64_t pos = lower_bound32(tg.s_col, c0, c1, g);
-          if (pos < c1 && __ldg(tg.s_col + pos) == g) atomicAdd(tg.s_val + pos, __dmul_rn(pij, tb.lv[e]));
-          else atomicOr(status, ST_DRIFT);
+          row_ok = sr < tg.s_nrows && __ldg(tg.s_rows + sr) == Jg;
+          c0 = row_ok ? __ldg(tg.s_rp + sr) : 0; c1 = row_ok ? __ldg(tg.s_rp + sr + 1) : 0;
+          ccol = tg.s_col; cval = tg.s_val;
+        }
+        for (int64_t e = c0 + gl; e < c1; e += GROUP) {
+          int sl = table_find(tb.keys, log2t, __ldg(ccol + e));
+          if (sl >= 0) {
+            ++found;
+            atomicAdd(cval + e, __dmul_rn(pij, tb.vals[sl]));
+          }
         }
       }
+      found = group_sum<GROUP>(found);
+      if (live && found != n && gl == 0) atomicOr(status, ST_DRIFT);
     }
     __syncwarp();
   }
@@ -418,11 +436,11 @@ __global__ void k_merge_add(int64_t n, const int64_t *slot, const double *vals, 
 // ---------------------------------------------------------------------------
 // two-step: C~ = A P rows (structure sorted later), values onto structure
 // ---------------------------------------------------------------------------
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_ct_fill(Ops op, const int32_t *rows, unsigned long long nrows, int log2t,
                                                  unsigned char *gtables, const int64_t *ct_rp, int32_t *ct_col,
                                                  int *status) {
-  GroupTables tb = group_tables<GROUP, false>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, false, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -432,7 +450,7 @@ __global__ void __launch_bounds__(256) k_ct_fill(Ops op, const int32_t *rows, un
     unsigned long long ridx = r0 + lane_id() / GROUP;
     int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
     table_clear<GROUP>(tb.keys, T);
-    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, status);
+    ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, tb.ps, status);
     int n = table_compact<GROUP, false>(tb.keys, nullptr, T, tb.lk, nullptr);
     if (i >= 0) {
       int64_t b = ct_rp[i];
@@ -443,11 +461,11 @@ __global__ void __launch_bounds__(256) k_ct_fill(Ops op, const int32_t *rows, un
   }
 }
 
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_ct_numeric(Ops op, const int32_t *rows, unsigned long long nrows,
                                                     int log2t, unsigned char *gtables, const int64_t *ct_rp,
                                                     const int32_t *ct_col, double *ct_val, int *status) {
-  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, true, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(256) k_ct_numeric(Ops op, const int32_t *rows,
     unsigned long long ridx = r0 + lane_id() / GROUP;
     int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
     table_clear<GROUP>(tb.keys, T);
-    int nnew = ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, status);
+    int nnew = ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, tb.ps, status);
     nnew = group_sum<GROUP>(nnew);
     if (i >= 0) {
       int64_t b = ct_rp[i], L = ct_rp[i + 1] - b;
@@ -516,14 +534,14 @@ __global__ void k_ptc_symbolic(int64_t nrows, const int64_t *t_rp, const int32_t
 // two-step numeric rows of P^T C~ (src/_kernels.py:583-677): fold over the
 // transposed row's entries (ascending fine row) with C~ rows scattered per
 // step; then written onto the target structure (staging: set; C: 0 + acc).
-template <int GROUP>
+template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_ptc_numeric(const int32_t *rows, unsigned long long nrows, int log2t,
                                                      unsigned char *gtables, const int64_t *t_rp,
                                                      const int32_t *t_row, const double *t_val,
                                                      const int32_t *target_map, int64_t target_offset,
                                                      const int64_t *ct_rp, const int32_t *ct_col,
                                                      const double *ct_val, PtcTarget tg, int *status) {
-  GroupTables tb = group_tables<GROUP, true>(gtables, log2t);
+  GroupTables tb = group_tables<GROUP, true, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
@@ -748,19 +766,18 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 
 #define PTAP_ROWKERNEL_DISPATCH(KERNEL, NUM, ...)                                                         \
   do {                                                                                                     \
-    size_t gb = group_bytes(log2t, NUM);                                                                   \
-    if (group == 8) {                                                                                      \
+    if (gtables) {                                                                                         \
+      KERNEL<32, true><<<max_ctas, warps * 32, 0, stream>>>(__VA_ARGS__);                                  \
+    } else if (group == 8) {                                                                               \
       int gpc = warps * 4;                                                                                 \
-      size_t sm = gtables ? 0 : gb * gpc;                                                                  \
-      if ((e = set_smem(KERNEL<8>, sm)) != cudaSuccess) return e;                                          \
-      int grid = gtables ? max_ctas : grid_for(nrows, gpc, max_ctas);                                      \
-      KERNEL<8><<<grid, warps * 32, sm, stream>>>(__VA_ARGS__);                                            \
+      size_t sm = group_bytes(log2t, NUM, 8) * gpc;                                                        \
+      if ((e = set_smem(KERNEL<8, false>, sm)) != cudaSuccess) return e;                                   \
+      KERNEL<8, false><<<grid_for(nrows, gpc, max_ctas), warps * 32, sm, stream>>>(__VA_ARGS__);           \
     } else {                                                                                               \
       int gpc = warps;                                                                                     \
-      size_t sm = gtables ? 0 : gb * gpc;                                                                  \
-      if ((e = set_smem(KERNEL<32>, sm)) != cudaSuccess) return e;                                         \
-      int grid = gtables ? max_ctas : grid_for(nrows, gpc, max_ctas);                                      \
-      KERNEL<32><<<grid, warps * 32, sm, stream>>>(__VA_ARGS__);                                           \
+      size_t sm = group_bytes(log2t, NUM, 32) * gpc;                                                       \
+      if ((e = set_smem(KERNEL<32, false>, sm)) != cudaSuccess) return e;                                  \
+      KERNEL<32, false><<<grid_for(nrows, gpc, max_ctas), warps * 32, sm, stream>>>(__VA_ARGS__);          \
     }                                                                                                      \
     return cudaGetLastError();                                                                             \
   } while (0)
@@ -821,7 +838,7 @@ cudaError_t launch_ptc_numeric(const LaunchShape &s, const int32_t *rows, unsign
                           target_offset, ct_rp, ct_col, ct_val, tg, status);
 }
 
-size_t row_kernel_group_bytes(int log2t, bool num) { return group_bytes(log2t, num); }
+size_t row_kernel_group_bytes(int log2t, bool num, int group) { return group_bytes(log2t, num, group); }
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 

@@ -47,7 +47,7 @@ struct LaunchShape {
   unsigned char *gtables;  // non-null: tables in global memory (one per group of the capped grid)
 };
 
-size_t row_kernel_group_bytes(int log2t, bool num);
+size_t row_kernel_group_bytes(int log2t, bool num, int group);
 
 cudaError_t launch_row_work(const Ops &op, int64_t *apub, unsigned long long *mac, cudaStream_t st);
 cudaError_t launch_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_rp, const int64_t *po_rp, int mode,
