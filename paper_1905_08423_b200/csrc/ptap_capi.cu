@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -83,7 +84,12 @@ struct ptap_plan {
   BinSet bins_send, bins_local, bins_all, bins_ptd, bins_pto;
   // transient state carried from symbolic_send to symbolic_local
   int64_t *ap_nnz = nullptr;
+  int64_t *apub = nullptr;
   Arena local_arena{nullptr, 0};
+  // plan-mapped numeric (all-at-once / merged)
+  bool mapped = false;
+  MapArgs maps{};
+  int64_t smap_bytes = 0, pmap_bytes = 0;
   unsigned long long bound_local = 0, bound_send = 0, sum_ap = 0;
   // C
   int64_t c_nnz = 0;
@@ -407,7 +413,7 @@ ptap_status build_transpose(ptap_plan *p, Transpose &t, int64_t ntrows, const in
   return PTAP_OK;
 }
 
-ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStream_t st) {
+ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStream_t st, int64_t **apub_out = nullptr) {
   int64_t *apub = nullptr, *ap_nnz = nullptr;
   CKS(palloc(p, &apub, op.nloc, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(p->d_u64 + 7, 0, sizeof(unsigned long long), st));
@@ -423,7 +429,7 @@ ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStre
     return launch_ap_count(s, op, rows, n, ap_nnz, p->d_status, st);
   }));
   free_bins(p, tmp, st);
-  pfree(p, apub, st);
+  if (apub_out) *apub_out = apub; else pfree(p, apub, st);
   // bounds of the outer products
   CK(cudaMemsetAsync(p->d_u64 + 8, 0, 3 * sizeof(unsigned long long), st));
   CK(launch_outer_bounds(op.nloc, op.pd_rp, op.po_rp, ap_nnz, p->d_u64 + 8, st));
@@ -462,6 +468,76 @@ ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
     CKS(arena_grow(p, ar, st));
   }
   return fail(PTAP_ERR_OOM, "symbolic arena kept overflowing");
+}
+
+// Plan-mapped numeric: byte maps of slots (AP row) and positions (target rows)
+// computed once here so numeric passes do no hashing and no searching.
+ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  p->mapped = false;
+  unsigned long long *mx = p->d_u64 + 12;
+  CK(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), st));
+  CK(launch_max_i64(p->nloc, p->ap_nnz, mx, st));
+  CK(launch_max_rowlen(p->ncl, p->c_rp, mx + 1, st));
+  if (p->s_nrows) CK(launch_max_rowlen(p->s_nrows, p->s_rp, mx + 2, st));
+  unsigned long long h[3];
+  CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->cnt.kernel_launches += 3;
+  if (h[0] > 255 || h[1] > 256 || h[2] > 256) return PTAP_OK;  // hash path for this plan
+  int64_t *slen = nullptr, *plen = nullptr, *scratch = nullptr;
+  CKS(palloc(p, &slen, p->nloc, CAT_TRANSIENT, st));
+  CKS(palloc(p, &plen, p->nloc, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
+  CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, slen, plen, st));
+  CKS(palloc(p, &p->maps.smap_rp, p->nloc + 1, CAT_PLAN, st));
+  CKS(palloc(p, &p->maps.pmap_rp, p->nloc + 1, CAT_PLAN, st));
+  CK(scan_exclusive(slen, p->maps.smap_rp, p->nloc, scratch, st));
+  CK(scan_exclusive(plen, p->maps.pmap_rp, p->nloc, scratch, st));
+  int64_t tot[2];
+  CK(cudaMemcpyAsync(&tot[0], p->maps.smap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], p->maps.pmap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  pfree(p, slen, st);
+  pfree(p, plen, st);
+  pfree(p, scratch, st);
+  p->smap_bytes = tot[0];
+  p->pmap_bytes = tot[1];
+  CKS(palloc(p, &p->maps.smap, tot[0], CAT_PLAN, st));
+  CKS(palloc(p, &p->maps.pmap, tot[1], CAT_PLAN, st));
+  CKS(palloc(p, &p->maps.nap, p->nloc, CAT_PLAN, st));
+  int64_t po_nnz = ops->p_off.nnz;
+  CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
+  if (po_nnz > 0) CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
+  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+  CK(launch_build_maps(op, nullptr, (unsigned long long)p->nloc, p->maps, tg, p->d_status, st));
+  p->cnt.kernel_launches += 5;
+  p->mapped = true;
+  return PTAP_OK;
+}
+
+ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
+  pfree(p, p->maps.smap_rp, st); pfree(p, p->maps.pmap_rp, st);
+  pfree(p, p->maps.smap, st); pfree(p, p->maps.pmap, st);
+  pfree(p, p->maps.nap, st); pfree(p, p->maps.po_srow, st);
+  p->mapped = false;
+  return PTAP_OK;
+}
+
+ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_send, int do_local, cudaStream_t st) {
+  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+  if (p->mapped) {
+    for (int q = 0; q < NBINS; ++q) {
+      if (bs.count[q] == 0) continue;
+      const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
+      CK(launch_outer_numeric_mapped(q == 0 ? 0 : 1, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
+                                     do_local, p->d_status, st));
+      p->cnt.kernel_launches++;
+    }
+    return PTAP_OK;
+  }
+  return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+    return launch_outer_numeric(s, op, rows, n, do_send, do_local, tg, p->d_status, st);
+  });
 }
 
 }  // namespace
@@ -510,7 +586,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
-  CKS(ap_sizes(p, op, &p->ap_nnz, st));
+  CKS(ap_sizes(p, op, &p->ap_nnz, st, &p->apub));
   if (p->alg == PTAP_TWO_STEP) {
     // C~ = A P (src/spgemm.py:184-202), booked as auxiliary
     CKS(palloc(p, &p->ct_rp, p->nloc + 1, CAT_AUX, st));
@@ -665,7 +741,9 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
     pfree(p, est, st);
     p->cnt.kernel_launches += 2;
   }
+  if (p->alg != PTAP_TWO_STEP && !getenv("PTAP_NO_MAPS")) CKS(build_maps(p, op, ops, st));
   pfree(p, p->ap_nnz, st);
+  pfree(p, p->apub, st);
   int s = 0;
   CKS(read_status(p, st, &s));
   if (s & ST_DRIFT) {
@@ -707,11 +785,8 @@ ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stre
   bool merged = p->alg == PTAP_MERGED;
   if (p->s_nnz > 0) CK(cudaMemsetAsync(p->s_val, 0, sizeof(double) * p->s_nnz, st));
   if (merged && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
-  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   BinSet &bs = merged ? p->bins_all : p->bins_send;
-  CKS(for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
-    return launch_outer_numeric(s, op, rows, n, 1, merged ? 1 : 0, tg, p->d_status, st);
-  }));
+  CKS(run_outer_numeric(p, op, bs, 1, merged ? 1 : 0, st));
   p->cnt.numeric_row_kernel_calls += bs.selected;
   return PTAP_OK;
 }
@@ -729,10 +804,7 @@ ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *str
     p->cnt.numeric_row_kernel_calls += p->nloc;
   } else if (p->alg == PTAP_ALLATONCE) {
     if (p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
-    OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
-    CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
-      return launch_outer_numeric(s, op, rows, n, 0, 1, tg, p->d_status, st);
-    }));
+    CKS(run_outer_numeric(p, op, p->bins_local, 0, 1, st));
     p->cnt.numeric_row_kernel_calls += p->bins_local.selected;
   }
   p->cnt.numeric_runs++;
@@ -784,6 +856,7 @@ ptap_status ptap_plan_release_cache(ptap_plan *p) {
   free_bins(p, p->bins_pto, st);
   pfree(p, p->s_rows, st); pfree(p, p->s_rp, st); pfree(p, p->s_col, st); pfree(p, p->s_val, st);
   pfree(p, p->r_slot, st);
+  free_maps(p, st);
   pfree(p, p->ct_rp, st); pfree(p, p->ct_col, st); pfree(p, p->ct_val, st);
   for (Transpose *t : {&p->ptd, &p->pto}) {
     pfree(p, t->rp, st); pfree(p, t->row, st); pfree(p, t->perm, st); pfree(p, t->val, st);

@@ -39,6 +39,16 @@ struct PtcTarget {
   double *val;
 };
 
+// plan-mapped numeric (ptap_mapped.cu)
+struct MapArgs {
+  int64_t *smap_rp;  // [nloc+1] offsets into smap
+  uint8_t *smap;     // slot of every (A entry, P entry) pair, fold order
+  int64_t *pmap_rp;  // [nloc+1] offsets into pmap
+  uint8_t *pmap;     // position of every slot in every target row of P(i,:)
+  uint8_t *nap;      // [nloc] AP row sizes
+  int32_t *po_srow;  // [nnz(P_o)] staging row of every P_o entry
+};
+
 struct LaunchShape {
   int group;     // 8 or 32 lanes per row
   int warps;     // warps per CTA
@@ -108,5 +118,16 @@ cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t tar
                            int64_t t_nrows, const int32_t *t_rows, const int64_t *t_rp, int64_t *est,
                            cudaStream_t st);
 cudaError_t launch_touch(void *buf, int64_t bytes, cudaStream_t st);
+cudaError_t launch_map_lengths(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *apub,
+                               const int64_t *ap_nnz, int64_t *slen, int64_t *plen, cudaStream_t st);
+cudaError_t launch_po_srow(int64_t nnz, const int32_t *po_col, const int32_t *colmap, int64_t s_nrows,
+                           const int32_t *s_rows, int32_t *po_srow, int *status, cudaStream_t st);
+cudaError_t launch_max_i64(int64_t n, const int64_t *v, unsigned long long *mx, cudaStream_t st);
+cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *mx, cudaStream_t st);
+cudaError_t launch_build_maps(const Ops &op, const int32_t *rows, unsigned long long nrows, const MapArgs &mp,
+                              const OuterTargets &tg, int *status, cudaStream_t st);
+cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                        const MapArgs &mp, const OuterTargets &tg, int do_send, int do_local,
+                                        int *status, cudaStream_t st);
 
 }  // namespace ptapdev

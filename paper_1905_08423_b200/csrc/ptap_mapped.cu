@@ -1,0 +1,379 @@
+// ptap_mapped.cu -- plan-mapped numeric pass of the all-at-once / merged
+// triple product.
+//
+// The symbolic phase (k_build_maps) records, for every fine row i it will
+// process, two byte maps that make the numeric pass free of hashing and of
+// searches in C -- the "caching intermediate data" mode of the paper
+// (Table 6) applied to the outer-product algorithm:
+//
+//   smap[i]: for each (A entry, P entry) pair of row i, in the reference's
+//            fold order (A_d entries ascending, for each its P_d then P_o row;
+//            then A_o entries with the gathered rows, src/_kernels.py:205-227),
+//            the slot of the pair's column in AP(i,:) (slots = the row's
+//            columns in ascending order);
+//   pmap[i]: for each entry J of P(i,:) (P_d entries, then P_o entries) and
+//            each slot s, the position of AP(i,:)'s s-th column inside the
+//            target row (the local C row J, or the staging row of J).
+//
+// The numeric kernel (k_outer_numeric_mapped) then folds AP(i,:) into a dense
+// per-row accumulator in the reference's order (one A entry per step, lanes
+// over its P row: conflict-free), and scatters P(i,J)*AP(i,s) to
+// C[row_start(J) + pmap] with fp64 atomics -- the outer product of
+// src/_kernels.py:446-515 without the per-entry binary searches (_c_slot,
+// :421-443).  Both maps are one byte per entry (rows with more than 255 AP
+// columns or C rows longer than 256 use the hash path instead).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptap_device.cuh"
+#include "ptap_kernels.cuh"
+
+namespace ptapdev {
+
+// lengths of the per-row maps (selected rows: P(i,:) nonempty)
+__global__ void k_map_lengths(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *apub,
+                              const int64_t *ap_nnz, int64_t *slen, int64_t *plen) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t np_ = pd_rp[i + 1] - pd_rp[i];
+  if (po_rp) np_ += po_rp[i + 1] - po_rp[i];
+  bool sel = np_ > 0;
+  slen[i] = sel ? apub[i] : 0;
+  plen[i] = sel ? np_ * ap_nnz[i] : 0;
+}
+
+// staging row of every P_o entry (global coarse column -> staging row index)
+__global__ void k_po_srow(int64_t nnz, const int32_t *po_col, const int32_t *colmap, int64_t s_nrows,
+                          const int32_t *s_rows, int32_t *po_srow, int *status) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  int32_t Jg = colmap[po_col[e]];
+  int64_t r = lower_bound32(s_rows, 0, s_nrows, Jg);
+  if (r >= s_nrows || s_rows[r] != Jg) { po_srow[e] = -1; atomicOr(status, ST_DRIFT); }
+  else po_srow[e] = (int32_t)r;
+}
+
+__global__ void k_max_i64(int64_t n, const int64_t *v, unsigned long long *mx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long x = i < n ? (unsigned long long)v[i] : 0;
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(FULL, x, o));
+  if (lane_id() == 0 && x) atomicMax(mx, x);
+}
+
+__global__ void k_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *mx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long x = i < n ? (unsigned long long)(rp[i + 1] - rp[i]) : 0;
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(FULL, x, o));
+  if (lane_id() == 0 && x) atomicMax(mx, x);
+}
+
+// ---------------------------------------------------------------------------
+// map builder: one warp per row (symbolic only)
+// ---------------------------------------------------------------------------
+constexpr int MAP_LOG2T = 9;  // 512-slot tables: up to 255 AP columns
+constexpr int MAP_T = 1 << MAP_LOG2T;
+
+__global__ void __launch_bounds__(256) k_build_maps(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                    MapArgs mp, OuterTargets tg, int *status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int wpc = blockDim.x >> 5;
+  // per warp: keys[T], lk[T/2], desc[256], slot_of[T], sortbuf[256]
+  unsigned char *base = smem + (size_t)warp * (MAP_T * 4 + (MAP_T / 2) * 4 + 256 * 4 + MAP_T * 4 + 256 * 4);
+  int32_t *keys = (int32_t *)base;
+  int32_t *lk = keys + MAP_T;
+  PStage ps;
+  ps.desc = lk + MAP_T / 2;
+  ps.a = nullptr;
+  int32_t *slot_of = ps.desc + 256;
+  int32_t *sb = slot_of + MAP_T;
+  for (unsigned long long r = (unsigned long long)blockIdx.x * wpc + warp; r < nrows;
+       r += (unsigned long long)gridDim.x * wpc) {
+    int64_t i = rows ? (int64_t)rows[r] : (int64_t)r;
+    int64_t pd0 = op.pd_rp[i], pd1 = op.pd_rp[i + 1], po0 = 0, po1 = 0;
+    if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
+    int ndP = (int)(pd1 - pd0), nP = ndP + (int)(po1 - po0);
+    if (nP == 0) continue;  // warp-uniform (one row per warp)
+    table_clear<32>(keys, MAP_T);
+    ap_row_accumulate<32, false>(op, i, keys, nullptr, MAP_LOG2T, ps, status);
+    int n = table_compact<32, false>(keys, nullptr, MAP_T, lk, nullptr);
+    if (n > 255) {
+      if (lane == 0) atomicOr(status, ST_TABLE_FULL);
+      continue;
+    }
+    // sort the row's columns: slot = rank
+    int P2 = 1;
+    while (P2 < n) P2 <<= 1;
+    for (int x = lane; x < P2; x += 32) sb[x] = x < n ? lk[x] : INT32_MAX;
+    __syncwarp();
+    for (int k = 2; k <= P2; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int x = lane; x < P2; x += 32) {
+          int y = x ^ j;
+          if (y > x) {
+            bool up = (x & k) == 0;
+            int32_t kx = sb[x], ky = sb[y];
+            if ((kx > ky) == up) { sb[x] = ky; sb[y] = kx; }
+          }
+        }
+        __syncwarp();
+      }
+    for (int x = lane; x < n; x += 32) slot_of[table_find(keys, MAP_LOG2T, sb[x])] = x;
+    __syncwarp();
+    if (lane == 0) mp.nap[i] = (uint8_t)n;
+    // smap: pairs in fold order
+    int64_t run = mp.smap_rp[i];
+    for (int src = 0; src < 2; ++src) {
+      const int64_t *arp = src ? op.ao_rp : op.ad_rp;
+      if (!arp) continue;
+      const int32_t *acol = src ? op.ao_col : op.ad_col;
+      for (int64_t t = arp[i]; t < arp[i + 1]; ++t) {
+        int32_t k = acol[t];
+        int64_t d0, d1, o0 = 0, o1 = 0;
+        if (src == 0) {
+          d0 = op.pd_rp[k]; d1 = op.pd_rp[k + 1];
+          if (op.po_rp) { o0 = op.po_rp[k]; o1 = op.po_rp[k + 1]; }
+        } else {
+          d0 = op.pr_rp[k]; d1 = op.pr_rp[k + 1];
+        }
+        int nd = (int)(d1 - d0), plen = nd + (int)(o1 - o0);
+        for (int u = lane; u < plen; u += 32) {
+          int32_t g;
+          if (u < nd) g = src ? op.pr_col[d0 + u] : op.pd_col[d0 + u] + (int32_t)op.c_lo;
+          else g = op.p_colmap[op.po_col[o0 + (u - nd)]];
+          int h = table_find(keys, MAP_LOG2T, g);
+          mp.smap[run + u] = (uint8_t)(h >= 0 ? slot_of[h] : 0);
+          if (h < 0) atomicOr(status, ST_DRIFT);
+        }
+        run += plen;
+      }
+    }
+    // pmap: every target row of P(i,:)
+    int64_t pb = mp.pmap_rp[i];
+    for (int jj = 0; jj < nP; ++jj) {
+      int64_t c0, c1;
+      const int32_t *ccol;
+      if (jj < ndP) {
+        int32_t J = op.pd_col[pd0 + jj];
+        c0 = tg.c_rp[J]; c1 = tg.c_rp[J + 1]; ccol = tg.c_col;
+      } else {
+        int32_t sr = mp.po_srow[po0 + (jj - ndP)];
+        if (sr < 0) { if (lane == 0) atomicOr(status, ST_DRIFT); continue; }
+        c0 = tg.s_rp[sr]; c1 = tg.s_rp[sr + 1]; ccol = tg.s_col;
+      }
+      int found = 0;
+      for (int64_t e = c0 + lane; e < c1; e += 32) {
+        int h = table_find(keys, MAP_LOG2T, ccol[e]);
+        if (h >= 0) { mp.pmap[pb + (int64_t)jj * n + slot_of[h]] = (uint8_t)(e - c0); ++found; }
+      }
+      for (int o = 16; o > 0; o >>= 1) found += __shfl_xor_sync(FULL, found, o);
+      if (found != n && lane == 0) atomicOr(status, ST_DRIFT);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// numeric: G lanes per row; 32/G rows per warp
+// ---------------------------------------------------------------------------
+template <int G, int NAPCAP>
+__global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                              MapArgs mp, OuterTargets tg, int do_send, int do_local,
+                                                              int *status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = lane_id(), gl = lane & (G - 1);
+  const int gpw = 32 / G;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int gid = (threadIdx.x >> 5) * gpw + lane / G;
+  // per group: acc[NAPCAP] (f64), ent_a[G] (f64), ent_d0[G], ent_o0[G], ent_ndpl[G], ent_off[G] (i32)
+  const size_t gbytes = (size_t)NAPCAP * 8 + G * 8 + G * 16;
+  unsigned char *gbase = smem + (size_t)gid * gbytes;
+  double *acc = (double *)gbase;
+  double *ent_a = acc + NAPCAP;
+  int32_t *ent_d0 = (int32_t *)(ent_a + G);
+  int32_t *ent_o0 = ent_d0 + G;
+  int32_t *ent_ndpl = ent_o0 + G;
+  int32_t *ent_off = ent_ndpl + G;
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane / G;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    int64_t pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
+    if (i >= 0) {
+      pd0 = __ldg(op.pd_rp + i); pd1 = __ldg(op.pd_rp + i + 1);
+      if (op.po_rp) { po0 = __ldg(op.po_rp + i); po1 = __ldg(op.po_rp + i + 1); }
+    }
+    bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
+    if (!(wl || ws)) i = -1;
+    if (__all_sync(FULL, i < 0)) continue;
+    int nap = i >= 0 ? (int)__ldg(mp.nap + i) : 0;
+    for (int s = gl; s < nap; s += G) acc[s] = 0.0;
+    int64_t sbase = i >= 0 ? __ldg(mp.smap_rp + i) : 0;
+    const uint8_t *smap = mp.smap + sbase;
+    int run = 0;
+    __syncwarp();
+#pragma unroll 1
+    for (int src = 0; src < 2; ++src) {
+      const int64_t *arp = src ? op.ao_rp : op.ad_rp;
+      if (arp == nullptr) continue;
+      const int32_t *acol = src ? op.ao_col : op.ad_col;
+      const double *aval = src ? op.ao_val : op.ad_val;
+      const double *qval = src ? op.pr_val : op.pd_val;
+      int64_t t0 = 0, t1 = 0;
+      if (i >= 0) { t0 = __ldg(arp + i); t1 = __ldg(arp + i + 1); }
+      int len = (int)(t1 - t0);
+      int maxlen = __reduce_max_sync(FULL, len);
+#pragma unroll 1
+      for (int tb = 0; tb < maxlen; tb += G) {
+        int t = tb + gl;
+        double a = 0.0;
+        int32_t d0 = 0, o0 = 0;
+        int nd = 0, plen = 0;
+        if (t < len) {
+          int32_t k = __ldg(acol + t0 + t);
+          a = __ldg(aval + t0 + t);
+          if (src == 0) {
+            int64_t x0 = __ldg(op.pd_rp + k);
+            d0 = (int32_t)x0;
+            nd = (int)(__ldg(op.pd_rp + k + 1) - x0);
+            plen = nd;
+            if (op.po_rp) { int64_t y0 = __ldg(op.po_rp + k); o0 = (int32_t)y0; plen += (int)(__ldg(op.po_rp + k + 1) - y0); }
+          } else {
+            int64_t x0 = __ldg(op.pr_rp + k);
+            d0 = (int32_t)x0;
+            nd = plen = (int)(__ldg(op.pr_rp + k + 1) - x0);
+          }
+        }
+        int incl = plen;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+          int y = __shfl_up_sync(FULL, incl, o, G);
+          if (gl >= o) incl += y;
+        }
+        ent_a[gl] = a; ent_d0[gl] = d0; ent_o0[gl] = o0; ent_ndpl[gl] = nd | (plen << 16); ent_off[gl] = run + incl - plen;
+        int ctot = __shfl_sync(FULL, incl, G - 1, G);
+        __syncwarp();
+        int steps = min(G, maxlen - tb);
+#pragma unroll 1
+        for (int j = 0; j < steps; ++j) {
+          int ndpl = ent_ndpl[j];
+          int ndj = ndpl & 0xffff, plj = ndpl >> 16;
+          double aj = ent_a[j];
+          int32_t d0j = ent_d0[j];
+          const uint8_t *sm = smap + ent_off[j];
+          for (int u = gl; u < plj; u += G) {
+            double p = u < ndj ? __ldg(qval + d0j + u) : __ldg(op.po_val + ent_o0[j] + (u - ndj));
+            int s = __ldg(sm + u);
+            acc[s] = __dadd_rn(acc[s], __dmul_rn(aj, p));
+          }
+          __syncwarp();
+        }
+        run += ctot;
+      }
+    }
+    // outer products into C (local rows) and the staging (send rows)
+    int ndP = (int)(pd1 - pd0);
+    int nP = ndP + (int)(po1 - po0);
+    int maxj = __reduce_max_sync(FULL, i >= 0 ? nP : 0);
+    int64_t pbase = i >= 0 ? __ldg(mp.pmap_rp + i) : 0;
+    for (int jj = 0; jj < maxj; ++jj) {
+      bool live = i >= 0 && jj < nP && (jj < ndP ? wl : ws);
+      if (live) {
+        double pij;
+        int64_t base;
+        double *cval;
+        if (jj < ndP) {
+          int32_t J = __ldg(op.pd_col + pd0 + jj);
+          pij = __ldg(op.pd_val + pd0 + jj);
+          base = __ldg(tg.c_rp + J);
+          cval = tg.c_val;
+        } else {
+          int64_t e = po0 + (jj - ndP);
+          pij = __ldg(op.po_val + e);
+          base = __ldg(tg.s_rp + __ldg(mp.po_srow + e));
+          cval = tg.s_val;
+        }
+        const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
+        for (int s = gl; s < nap; s += G) {
+          int pos = __ldg(pm + s);
+          atomicAdd(cval + base + pos, __dmul_rn(pij, acc[s]));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename K>
+static cudaError_t opt_in(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
+
+cudaError_t launch_map_lengths(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *apub,
+                               const int64_t *ap_nnz, int64_t *slen, int64_t *plen, cudaStream_t st) {
+  if (n > 0) k_map_lengths<<<nb(n, 256), 256, 0, st>>>(n, pd_rp, po_rp, apub, ap_nnz, slen, plen);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_po_srow(int64_t nnz, const int32_t *po_col, const int32_t *colmap, int64_t s_nrows,
+                           const int32_t *s_rows, int32_t *po_srow, int *status, cudaStream_t st) {
+  if (nnz > 0) k_po_srow<<<nb(nnz, 256), 256, 0, st>>>(nnz, po_col, colmap, s_nrows, s_rows, po_srow, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_i64(int64_t n, const int64_t *v, unsigned long long *mx, cudaStream_t st) {
+  if (n > 0) k_max_i64<<<nb(n, 256), 256, 0, st>>>(n, v, mx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *mx, cudaStream_t st) {
+  if (n > 0) k_max_rowlen<<<nb(n, 256), 256, 0, st>>>(n, rp, mx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_maps(const Ops &op, const int32_t *rows, unsigned long long nrows, const MapArgs &mp,
+                              const OuterTargets &tg, int *status, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  const int warps = 4;
+  size_t sm = (size_t)warps * (MAP_T * 4 + (MAP_T / 2) * 4 + 256 * 4 + MAP_T * 4 + 256 * 4);
+  cudaError_t e = opt_in(k_build_maps, sm);
+  if (e != cudaSuccess) return e;
+  unsigned long long grid = (nrows + warps - 1) / warps;
+  if (grid > 148ull * 64) grid = 148ull * 64;
+  k_build_maps<<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                        const MapArgs &mp, const OuterTargets &tg, int do_send, int do_local,
+                                        int *status, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  const int warps = 8;
+  cudaError_t e;
+  if (bin == 0) {
+    constexpr int G = 4, CAP = 32;
+    const int gpc = warps * (32 / G);
+    size_t sm = (size_t)gpc * (CAP * 8 + G * 8 + G * 16);
+    if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
+    unsigned long long grid = (nrows + gpc - 1) / gpc;
+    if (grid > 148ull * 64) grid = 148ull * 64;
+    k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
+                                                                    status);
+  } else {
+    constexpr int G = 32, CAP = 256;
+    const int gpc = warps;
+    size_t sm = (size_t)gpc * (CAP * 8 + G * 8 + G * 16);
+    if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
+    unsigned long long grid = (nrows + gpc - 1) / gpc;
+    if (grid > 148ull * 64) grid = 148ull * 64;
+    k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
+                                                                    status);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ptapdev
