@@ -24,6 +24,7 @@
 // columns or C rows longer than 256 use the hash path instead).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ptap_device.cuh"
@@ -122,7 +123,12 @@ __global__ void __launch_bounds__(256) k_build_maps(Ops op, const int32_t *rows,
     for (int x = lane; x < n; x += 32) slot_of[table_find(keys, MAP_LOG2T, sb[x])] = x;
     __syncwarp();
     if (lane == 0) mp.nap[i] = (uint8_t)n;
-    // smap: pairs in fold order
+    // smap: pairs in fold order; the first pair of every slot carries 0x80
+    // ("set" instead of "add": the reference's hm_add semantics, and no
+    // zero-fill of the accumulator) when the slot fits in 7 bits
+    const bool flag_first = n <= 127;
+    for (int x = lane; x < n; x += 32) sb[x] = 0;  // seen[slot]
+    __syncwarp();
     int64_t run = mp.smap_rp[i];
     for (int src = 0; src < 2; ++src) {
       const int64_t *arp = src ? op.ao_rp : op.ad_rp;
@@ -143,9 +149,14 @@ __global__ void __launch_bounds__(256) k_build_maps(Ops op, const int32_t *rows,
           if (u < nd) g = src ? op.pr_col[d0 + u] : op.pd_col[d0 + u] + (int32_t)op.c_lo;
           else g = op.p_colmap[op.po_col[o0 + (u - nd)]];
           int h = table_find(keys, MAP_LOG2T, g);
-          mp.smap[run + u] = (uint8_t)(h >= 0 ? slot_of[h] : 0);
+          int sl = h >= 0 ? slot_of[h] : 0;
+          int first = (flag_first && sb[sl] == 0) ? 0x80 : 0;
+          mp.smap[run + u] = (uint8_t)(sl | first);
           if (h < 0) atomicOr(status, ST_DRIFT);
         }
+        __syncwarp();
+        for (int u = lane; u < plen; u += 32) sb[mp.smap[run + u] & 0x7f] = 1;
+        __syncwarp();
         run += plen;
       }
     }
@@ -177,24 +188,29 @@ __global__ void __launch_bounds__(256) k_build_maps(Ops op, const int32_t *rows,
 // ---------------------------------------------------------------------------
 // numeric: G lanes per row; 32/G rows per warp
 // ---------------------------------------------------------------------------
+struct __align__(16) StepEntry {
+  double a;        // A value of the entry
+  int32_t d0;      // start of its P_d (or remote) row
+  uint32_t pk;     // pair offset (16 bits) | nd (8 bits) << 16 | plen (8 bits) << 24
+};
+
 template <int G, int NAPCAP>
 __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
                                                               MapArgs mp, OuterTargets tg, int do_send, int do_local,
                                                               int *status) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NREG = NAPCAP / G;  // accumulator slots owned per lane in the outer phase
   const int lane = lane_id(), gl = lane & (G - 1);
   const int gpw = 32 / G;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int gid = (threadIdx.x >> 5) * gpw + lane / G;
-  // per group: acc[NAPCAP] (f64), ent_a[G] (f64), ent_d0[G], ent_o0[G], ent_ndpl[G], ent_off[G] (i32)
-  const size_t gbytes = (size_t)NAPCAP * 8 + G * 8 + G * 16;
+  // per group: acc[NAPCAP + 1] (f64, +1 pad spreads groups over banks), ent[G], o0[G]
+  const size_t gbytes = ((((size_t)(NAPCAP + 1) * 8 + 15) & ~(size_t)15) + G * sizeof(StepEntry) + G * 4 + 15) & ~(size_t)15;
   unsigned char *gbase = smem + (size_t)gid * gbytes;
   double *acc = (double *)gbase;
-  double *ent_a = acc + NAPCAP;
-  int32_t *ent_d0 = (int32_t *)(ent_a + G);
-  int32_t *ent_o0 = ent_d0 + G;
-  int32_t *ent_ndpl = ent_o0 + G;
-  int32_t *ent_off = ent_ndpl + G;
+  StepEntry *ent = (StepEntry *)(gbase + (((size_t)(NAPCAP + 1) * 8 + 15) & ~(size_t)15));
+  int32_t *ent_o0 = (int32_t *)(ent + G);
+  const bool has_po = op.po_rp != nullptr;
   for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
        r0 += (unsigned long long)gridDim.x * gpc) {
     unsigned long long ridx = r0 + lane / G;
@@ -202,13 +218,14 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
     int64_t pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
     if (i >= 0) {
       pd0 = __ldg(op.pd_rp + i); pd1 = __ldg(op.pd_rp + i + 1);
-      if (op.po_rp) { po0 = __ldg(op.po_rp + i); po1 = __ldg(op.po_rp + i + 1); }
+      if (has_po) { po0 = __ldg(op.po_rp + i); po1 = __ldg(op.po_rp + i + 1); }
     }
     bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
     if (!(wl || ws)) i = -1;
     if (__all_sync(FULL, i < 0)) continue;
     int nap = i >= 0 ? (int)__ldg(mp.nap + i) : 0;
-    for (int s = gl; s < nap; s += G) acc[s] = 0.0;
+    if (nap > 127)  // no first-touch flags in the map: zero-fill
+      for (int s = gl; s < nap; s += G) acc[s] = 0.0;
     int64_t sbase = i >= 0 ? __ldg(mp.smap_rp + i) : 0;
     const uint8_t *smap = mp.smap + sbase;
     int run = 0;
@@ -219,7 +236,9 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
       if (arp == nullptr) continue;
       const int32_t *acol = src ? op.ao_col : op.ad_col;
       const double *aval = src ? op.ao_val : op.ad_val;
+      const int64_t *qrp = src ? op.pr_rp : op.pd_rp;
       const double *qval = src ? op.pr_val : op.pd_val;
+      const bool po_here = has_po && src == 0;
       int64_t t0 = 0, t1 = 0;
       if (i >= 0) { t0 = __ldg(arp + i); t1 = __ldg(arp + i + 1); }
       int len = (int)(t1 - t0);
@@ -227,22 +246,20 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
 #pragma unroll 1
       for (int tb = 0; tb < maxlen; tb += G) {
         int t = tb + gl;
-        double a = 0.0;
-        int32_t d0 = 0, o0 = 0;
+        StepEntry en;
+        en.a = 0.0; en.d0 = 0;
         int nd = 0, plen = 0;
+        int32_t o0 = 0;
         if (t < len) {
           int32_t k = __ldg(acol + t0 + t);
-          a = __ldg(aval + t0 + t);
-          if (src == 0) {
-            int64_t x0 = __ldg(op.pd_rp + k);
-            d0 = (int32_t)x0;
-            nd = (int)(__ldg(op.pd_rp + k + 1) - x0);
-            plen = nd;
-            if (op.po_rp) { int64_t y0 = __ldg(op.po_rp + k); o0 = (int32_t)y0; plen += (int)(__ldg(op.po_rp + k + 1) - y0); }
-          } else {
-            int64_t x0 = __ldg(op.pr_rp + k);
-            d0 = (int32_t)x0;
-            nd = plen = (int)(__ldg(op.pr_rp + k + 1) - x0);
+          en.a = __ldg(aval + t0 + t);
+          int64_t x0 = __ldg(qrp + k);
+          en.d0 = (int32_t)x0;
+          nd = plen = (int)(__ldg(qrp + k + 1) - x0);
+          if (po_here) {
+            int64_t y0 = __ldg(op.po_rp + k);
+            o0 = (int32_t)y0;
+            plen += (int)(__ldg(op.po_rp + k + 1) - y0);
           }
         }
         int incl = plen;
@@ -251,27 +268,37 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
           int y = __shfl_up_sync(FULL, incl, o, G);
           if (gl >= o) incl += y;
         }
-        ent_a[gl] = a; ent_d0[gl] = d0; ent_o0[gl] = o0; ent_ndpl[gl] = nd | (plen << 16); ent_off[gl] = run + incl - plen;
+        en.pk = (uint32_t)(run + incl - plen) | ((uint32_t)nd << 16) | ((uint32_t)plen << 24);
+        ent[gl] = en;
+        if (po_here) ent_o0[gl] = o0;
         int ctot = __shfl_sync(FULL, incl, G - 1, G);
         __syncwarp();
         int steps = min(G, maxlen - tb);
 #pragma unroll 1
         for (int j = 0; j < steps; ++j) {
-          int ndpl = ent_ndpl[j];
-          int ndj = ndpl & 0xffff, plj = ndpl >> 16;
-          double aj = ent_a[j];
-          int32_t d0j = ent_d0[j];
-          const uint8_t *sm = smap + ent_off[j];
-          for (int u = gl; u < plj; u += G) {
-            double p = u < ndj ? __ldg(qval + d0j + u) : __ldg(op.po_val + ent_o0[j] + (u - ndj));
-            int s = __ldg(sm + u);
-            acc[s] = __dadd_rn(acc[s], __dmul_rn(aj, p));
+          const StepEntry ej = ent[j];  // one 16-byte shared load per step
+          int plj = (int)(ej.pk >> 24);
+          if (gl < plj) {
+            int ndj = (int)((ej.pk >> 16) & 0xff);
+            const uint8_t *sm = smap + (ej.pk & 0xffff);
+            for (int u = gl; u < plj; u += G) {
+              double p = u < ndj ? __ldg(qval + ej.d0 + u) : __ldg(op.po_val + ent_o0[j] + (u - ndj));
+              int s = __ldg(sm + u);
+              double prod = __dmul_rn(ej.a, p);
+              int sl = s & 0x7f;
+              if (nap > 127) sl = s;
+              acc[sl] = (nap <= 127 && (s & 0x80)) ? prod : __dadd_rn(acc[sl], prod);
+            }
           }
           __syncwarp();
         }
         run += ctot;
       }
     }
+    // accumulator slots of this lane into registers (slot = gl + G*r)
+    double accr[NREG];
+#pragma unroll
+    for (int r = 0; r < NREG; ++r) accr[r] = (gl + G * r < nap) ? acc[gl + G * r] : 0.0;
     // outer products into C (local rows) and the staging (send rows)
     int ndP = (int)(pd1 - pd0);
     int nP = ndP + (int)(po1 - po0);
@@ -295,9 +322,10 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
           cval = tg.s_val;
         }
         const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
-        for (int s = gl; s < nap; s += G) {
-          int pos = __ldg(pm + s);
-          atomicAdd(cval + base + pos, __dmul_rn(pij, acc[s]));
+#pragma unroll
+        for (int r = 0; r < NREG; ++r) {
+          int s = gl + G * r;
+          if (s < nap) atomicAdd(cval + base + __ldg(pm + s), __dmul_rn(pij, accr[r]));
         }
       }
     }
@@ -309,6 +337,18 @@ template <typename K>
 static cudaError_t opt_in(K kern, size_t bytes) {
   if (bytes > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   return cudaSuccess;
+}
+
+// no more CTAs than can be resident: the rows in flight form one contiguous
+// band, so the gathered P rows and the touched C rows stay in L2
+template <typename K>
+static unsigned long long resident(K kern, int threads, size_t smem) {
+  int dev = 0, nsm = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return (unsigned long long)nsm * per_sm;
 }
 
 static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
@@ -357,7 +397,7 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
   if (bin == 0) {
     constexpr int G = 4, CAP = 32;
     const int gpc = warps * (32 / G);
-    size_t sm = (size_t)gpc * (CAP * 8 + G * 8 + G * 16);
+    size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
     if (grid > 148ull * 64) grid = 148ull * 64;
@@ -366,7 +406,7 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
   } else {
     constexpr int G = 32, CAP = 256;
     const int gpc = warps;
-    size_t sm = (size_t)gpc * (CAP * 8 + G * 8 + G * 16);
+    size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
     if (grid > 148ull * 64) grid = 148ull * 64;
