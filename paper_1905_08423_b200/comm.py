@@ -104,7 +104,9 @@ def init_from_env(backend: str | None = None) -> RankContext:
             torch.cuda.set_device(local)
         return single_rank_context()
     if backend is None:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # PTAP_BACKEND=gloo runs several ranks on one GPU (functional checks of
+        # the multi-rank path when only one device is available)
+        backend = os.environ.get("PTAP_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
     if torch.cuda.is_available():
         ndev = torch.cuda.device_count()
         torch.cuda.set_device(local % ndev)
