@@ -300,6 +300,12 @@ def our_arm(args):
         return plan, max_over_ranks(time.perf_counter() - t, ctx, torch)
 
     # --- headline: all-at-once ------------------------------------------------
+    plan, sym_cold = symbolic("allatonce")   # first call: includes one-time module/pool setup
+    del plan
+    import gc
+
+    gc.collect()
+    torch.cuda.synchronize()
     plan, sym_s = symbolic("allatonce")
     cnt = plan.device_counters()
     mac = sum_over_ranks(cnt["mac_ap"] + cnt["mac_outer"], ctx, torch)
@@ -317,7 +323,7 @@ def our_arm(args):
     traffic, ncu_meta = ncu_traffic()
     kms = statistics.mean(kern_ms) if kern_ms else ms
     achieved = my_bytes / (kms * 1e-3) / 1e9
-    out["allatonce"] = {"numeric_ms": ms, "symbolic_ms": sym_s * 1e3,
+    out["allatonce"] = {"numeric_ms": ms, "symbolic_ms": sym_s * 1e3, "symbolic_cold_ms": sym_cold * 1e3,
                         "aux_peak_bytes": mem["device_high_water"] - mem["current"]["output_matrix"],
                         "memory": mem}
 
@@ -331,7 +337,8 @@ def our_arm(args):
                         "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
                         "memory": vmem}
             del vplan
-            torch.cuda.empty_cache()
+            gc.collect()
+            torch.cuda.synchronize()
 
     # --- config 3 level 2: A2 = C1 (device-resident chain), P2 trilinear ---------
     level2 = None

@@ -10,6 +10,7 @@
 //   plan_cache           bin row lists, all-at-once staging, received-slot map, transpose permutations
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -32,6 +33,19 @@ ptap_status fail(ptap_status s, const std::string &msg) {
 }
 
 enum Cat { CAT_INPUT = 0, CAT_OUTPUT = 1, CAT_AUX = 2, CAT_TRANSIENT = 3, CAT_PLAN = 4 };
+
+// PTAP_TRACE=1: synchronise and print the wall time of each symbolic step
+struct Tracer {
+  bool on = getenv("PTAP_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(cudaStream_t st, const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ptap] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 
 #define CK(x)                                                                                            \
   do {                                                                                                   \
@@ -88,7 +102,11 @@ struct ptap_plan {
   Arena local_arena{nullptr, 0};
   // plan-mapped numeric (all-at-once / merged)
   bool mapped = false;
+  bool want_maps = false;
   MapArgs maps{};
+  MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
+  int64_t *pat_rp = nullptr;
+  int32_t *pat = nullptr;
   int64_t smap_bytes = 0, pmap_bytes = 0;
   unsigned long long bound_local = 0, bound_send = 0, sum_ap = 0;
   // C
@@ -219,9 +237,9 @@ LaunchShape shape_for(int q, const BinSet &bs) {
   s.gtables = nullptr;
   s.max_ctas = 148 * 64;
   switch (q) {
-    case 0: s.group = 8; s.warps = 8; s.log2t = 6; break;
-    case 1: s.group = 32; s.warps = 8; s.log2t = 9; break;
-    case 2: s.group = 32; s.warps = 2; s.log2t = 12; break;
+    case 0: s.group = 8; s.warps = 8; s.log2t = 6; break;   // <= 32 keys
+    case 1: s.group = 8; s.warps = 8; s.log2t = 8; break;   // <= 128 keys
+    case 2: s.group = 32; s.warps = 2; s.log2t = 11; break; // <= 1024 keys
     default:
       s.group = 32; s.warps = 4; s.log2t = bs.log2t_global; s.max_ctas = 148 * 2; s.gtables = bs.gtables;
   }
@@ -472,46 +490,94 @@ ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
 
 // Plan-mapped numeric: byte maps of slots (AP row) and positions (target rows)
 // computed once here so numeric passes do no hashing and no searching.
-ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
-  p->mapped = false;
+// Plan-mapped numeric, part 1 (before the outer-product symbolic pass): the
+// slot maps are written by that pass itself, so allocate them here.
+ptap_status prepare_maps(ptap_plan *p, const Ops &op, cudaStream_t st) {
+  p->want_maps = false;
+  if (getenv("PTAP_NO_MAPS")) return PTAP_OK;
   unsigned long long *mx = p->d_u64 + 12;
   CK(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), st));
-  CK(launch_max_i64(p->nloc, p->ap_nnz, mx, st));
-  CK(launch_max_rowlen(p->ncl, p->c_rp, mx + 1, st));
-  if (p->s_nrows) CK(launch_max_rowlen(p->s_nrows, p->s_rp, mx + 2, st));
+  CK(launch_max_i64(p->nloc, p->ap_nnz, mx, st));      // AP row width  (slot byte)
+  CK(launch_max_i64(p->nloc, p->apub, mx + 1, st));    // pairs per row (16-bit offsets)
+  CK(launch_max_rowlen(p->nloc, op.pd_rp, mx + 2, st)); // P row length (8-bit counts)
   unsigned long long h[3];
   CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   p->cnt.kernel_launches += 3;
-  if (h[0] > 255 || h[1] > 256 || h[2] > 256) return PTAP_OK;  // hash path for this plan
-  int64_t *slen = nullptr, *plen = nullptr, *scratch = nullptr;
+  if (h[0] > 255 || h[1] > 65535 || h[2] > 255) return PTAP_OK;  // hash path for this plan
+  int64_t *slen = nullptr, *scratch = nullptr;
   CKS(palloc(p, &slen, p->nloc, CAT_TRANSIENT, st));
-  CKS(palloc(p, &plen, p->nloc, CAT_TRANSIENT, st));
   CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
-  CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, slen, plen, st));
+  int64_t *unused = nullptr;
+  CKS(palloc(p, &unused, p->nloc, CAT_TRANSIENT, st));
+  CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, slen, unused, st));
   CKS(palloc(p, &p->maps.smap_rp, p->nloc + 1, CAT_PLAN, st));
-  CKS(palloc(p, &p->maps.pmap_rp, p->nloc + 1, CAT_PLAN, st));
   CK(scan_exclusive(slen, p->maps.smap_rp, p->nloc, scratch, st));
-  CK(scan_exclusive(plen, p->maps.pmap_rp, p->nloc, scratch, st));
+  CKS(palloc(p, &p->pat_rp, p->nloc + 1, CAT_TRANSIENT, st));
+  CK(scan_exclusive(p->ap_nnz, p->pat_rp, p->nloc, scratch, st));
   int64_t tot[2];
   CK(cudaMemcpyAsync(&tot[0], p->maps.smap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tot[1], p->maps.pmap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], p->pat_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   pfree(p, slen, st);
-  pfree(p, plen, st);
+  pfree(p, unused, st);
   pfree(p, scratch, st);
   p->smap_bytes = tot[0];
-  p->pmap_bytes = tot[1];
   CKS(palloc(p, &p->maps.smap, tot[0], CAT_PLAN, st));
-  CKS(palloc(p, &p->maps.pmap, tot[1], CAT_PLAN, st));
   CKS(palloc(p, &p->maps.nap, p->nloc, CAT_PLAN, st));
-  int64_t po_nnz = ops->p_off.nnz;
-  CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
-  if (po_nnz > 0) CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
-  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
-  CK(launch_build_maps(op, nullptr, (unsigned long long)p->nloc, p->maps, tg, p->d_status, st));
-  p->cnt.kernel_launches += 5;
-  p->mapped = true;
+  CKS(palloc(p, &p->pat, tot[1], CAT_TRANSIENT, st));
+  p->mo = MapOut{p->maps.smap_rp, p->maps.smap, p->maps.nap, p->pat_rp, p->pat};
+  p->want_maps = true;
+  return PTAP_OK;
+}
+
+// Part 2 (C and the staging allocated): position maps, then drop the
+// transient patterns.  Falls back to the hash path if a target row is wider
+// than a byte can address.
+ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  p->mapped = false;
+  if (!p->want_maps) return PTAP_OK;
+  unsigned long long *mx = p->d_u64 + 12;
+  CK(cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), st));
+  CK(launch_max_rowlen(p->ncl, p->c_rp, mx, st));
+  if (p->s_nrows) CK(launch_max_rowlen(p->s_nrows, p->s_rp, mx + 1, st));
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  bool ok = h[0] <= 256 && h[1] <= 256;
+  if (ok) {
+    int64_t *plen = nullptr, *scratch = nullptr, *unused = nullptr;
+    CKS(palloc(p, &plen, p->nloc, CAT_TRANSIENT, st));
+    CKS(palloc(p, &unused, p->nloc, CAT_TRANSIENT, st));
+    CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
+    CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, unused, plen, st));
+    CKS(palloc(p, &p->maps.pmap_rp, p->nloc + 1, CAT_PLAN, st));
+    CK(scan_exclusive(plen, p->maps.pmap_rp, p->nloc, scratch, st));
+    int64_t tot = 0;
+    CK(cudaMemcpyAsync(&tot, p->maps.pmap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pfree(p, plen, st);
+    pfree(p, unused, st);
+    pfree(p, scratch, st);
+    p->pmap_bytes = tot;
+    CKS(palloc(p, &p->maps.pmap, tot, CAT_PLAN, st));
+    int64_t po_nnz = ops->p_off.nnz;
+    CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
+    if (po_nnz > 0)
+      CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
+    OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+    CK(launch_build_pmap(op, (unsigned long long)p->nloc, p->maps, p->mo, tg, p->d_status, st));
+    p->cnt.kernel_launches += 5;
+    p->mapped = true;
+  }
+  pfree(p, p->pat, st);
+  pfree(p, p->pat_rp, st);
+  p->mo = MapOut{};
+  if (!ok) {
+    pfree(p, p->maps.smap_rp, st);
+    pfree(p, p->maps.smap, st);
+    pfree(p, p->maps.nap, st);
+  }
   return PTAP_OK;
 }
 
@@ -552,6 +618,19 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
   if (!out) return fail(PTAP_ERR_VALUE, "null output");
   if (algorithm < 0 || algorithm > 2) return fail(PTAP_ERR_VALUE, "unknown algorithm");
   CKS(validate(ops));
+  static bool pool_configured = false;
+  if (!pool_configured) {
+    // keep freed device memory in the stream-ordered pool: repeated symbolic
+    // phases reuse it instead of going back to the driver
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_configured = true;
+  }
   ptap_plan *p = new ptap_plan();
   p->alg = algorithm;
   p->nloc = ops->n_local;
@@ -574,7 +653,8 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
 ptap_status ptap_plan_destroy(ptap_plan *p) {
   if (!p) return PTAP_OK;
   cudaDeviceSynchronize();
-  for (auto &kv : p->allocs) cudaFree(kv.first);
+  for (auto &kv : p->allocs) cudaFreeAsync(kv.first, 0);
+  cudaStreamSynchronize(0);
   cudaFree(p->d_status);
   cudaFree(p->d_u64);
   delete p;
@@ -586,7 +666,11 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
+  Tracer tr;
   CKS(ap_sizes(p, op, &p->ap_nnz, st, &p->apub));
+  tr.mark(st, "ap_sizes");
+  if (p->alg != PTAP_TWO_STEP) CKS(prepare_maps(p, op, st));
+  tr.mark(st, "prepare_maps");
   if (p->alg == PTAP_TWO_STEP) {
     // C~ = A P (src/spgemm.py:184-202), booked as auxiliary
     CKS(palloc(p, &p->ct_rp, p->nloc + 1, CAT_AUX, st));
@@ -642,7 +726,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     BinSet &bs = merged ? p->bins_all : p->bins_send;
     auto pass = [&]() -> ptap_status {
       return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
-        return launch_outer_symbolic(s, op, rows, n, 1, merged ? 1 : 0, p->local_arena, send, p->d_status, st);
+        return launch_outer_symbolic(s, op, rows, n, 1, merged ? 1 : 0, p->local_arena, send, p->mo, p->d_status, st);
       });
     };
     if (merged) {
@@ -662,8 +746,10 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     } else {
       CKS(with_arena_retry(p, send, st, pass));
     }
+    tr.mark(st, "outer symbolic (send/merged)");
     CKS(arena_to_staging(p, send, CAT_PLAN, st));
     pfree(p, send.keys, st);
+    tr.mark(st, "staging drain");
   }
   int s = 0;
   CKS(read_status(p, st, &s));
@@ -689,13 +775,15 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
   int64_t rnnz = recv ? recv->nnz : 0;
+  Tracer tr;
   if (p->alg != PTAP_MERGED) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st));
+  tr.mark(st, "local arena alloc");
   Arena &la = p->local_arena;
   if (p->alg == PTAP_ALLATONCE) {
     CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
       return for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
         Arena none{nullptr, 0};
-        return launch_outer_symbolic(s, op, rows, n, 0, 1, la, none, p->d_status, st);
+        return launch_outer_symbolic(s, op, rows, n, 0, 1, la, none, p->mo, p->d_status, st);
       });
     }));
     p->cnt.symbolic_row_kernel_calls += p->bins_local.selected;
@@ -719,8 +807,10 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
       return PTAP_OK;
     }));
   }
+  tr.mark(st, "local outer symbolic + recv");
   // allocate C (src/tripleproduct.py:203-212, src/spgemm.py:71-104)
   CKS(arena_to_csr(p, la, p->ncl, CAT_OUTPUT, &p->c_rp, &p->c_col, &p->c_nnz, nullptr, st));
+  tr.mark(st, "C drain + sort");
   pfree(p, la.keys, st);
   la = Arena{nullptr, 0};
   CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
@@ -741,7 +831,9 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
     pfree(p, est, st);
     p->cnt.kernel_launches += 2;
   }
-  if (p->alg != PTAP_TWO_STEP && !getenv("PTAP_NO_MAPS")) CKS(build_maps(p, op, ops, st));
+  tr.mark(st, "merge slots / two-step bins");
+  if (p->alg != PTAP_TWO_STEP) CKS(build_maps(p, op, ops, st));
+  tr.mark(st, "position maps");
   pfree(p, p->ap_nnz, st);
   pfree(p, p->apub, st);
   int s = 0;

@@ -132,127 +132,142 @@ __device__ __forceinline__ int table_find_or_claim(int32_t *keys, int log2t, int
   return -1;
 }
 
-// Row i of A*P accumulated by one lane group of GROUP lanes.  Fold order is
-// the reference's (src/_kernels.py:205-227): A_d entries ascending, then A_o
-// entries; for a key g the products are added left to right in that order,
-// the first product setting the slot (hm_add semantics, :116-147).
-//
-// The (A entry, P entry) pairs of a batch of GROUP A entries are flattened
-// (GROUP lanes each take a pair per round, so P rows are read coalesced and
-// every lane is busy), then the lanes of a round that carry the same key are
-// grouped with __match_any_sync: the lowest such lane folds the others' products
-// into the table value in lane (= pair) order.  Distinct rows of a warp use
-// distinct tables, so the match key carries the group id.
+// Row i of A*P accumulated by one lane group of GROUP lanes, in the
+// reference's fold order (src/_kernels.py:205-227): the A_d entries of row i
+// in ascending order, then the A_o entries.  One A entry per step: the
+// group's lanes scatter its P row (P_d entries, then P_o; columns distinct, so
+// a step is conflict-free) and a __syncwarp orders the steps.  The first
+// product for a key sets the slot, later ones add (hm_add, :116-147), each
+// rounded before the add.  Per chunk of GROUP A entries every lane loads one
+// entry and its P row bounds; the step then broadcasts them by shuffle.
 // i < 0 marks an idle group (it still joins every warp-collective).  Returns
 // (per lane) the number of new keys this lane created.
 template <int GROUP, bool NUM>
 __device__ __forceinline__ int ap_row_accumulate(const Ops &op, int64_t i, int32_t *keys, double *vals,
                                                  int log2t, const PStage &ps, int *status) {
-  const int lane = lane_id();
-  const int gl = lane & (GROUP - 1);
-  const unsigned gid = (unsigned)(lane / GROUP);
-  const int WIN = PAIRS_PER_LANE * GROUP;
+  const int gl = threadIdx.x & (GROUP - 1);
   int nnew = 0;
   bool ok = true;
+  const bool has_po = op.po_rp != nullptr;
 #pragma unroll 1
   for (int src = 0; src < 2; ++src) {
     const int64_t *arp = src ? op.ao_rp : op.ad_rp;
     if (arp == nullptr) continue;  // uniform
     const int32_t *acol = src ? op.ao_col : op.ad_col;
     const double *aval = src ? op.ao_val : op.ad_val;
+    const int64_t *qrp = src ? op.pr_rp : op.pd_rp;
     const int32_t *qcol = src ? op.pr_col : op.pd_col;
     const double *qval = src ? op.pr_val : op.pd_val;
     const int32_t coff = src ? 0 : (int32_t)op.c_lo;
+    const bool po_here = has_po && src == 0;
     int64_t t0 = 0, t1 = 0;
     if (i >= 0) { t0 = __ldg(arp + i); t1 = __ldg(arp + i + 1); }
     int len = (int)(t1 - t0);
     int maxlen = __reduce_max_sync(FULL, len);
 #pragma unroll 1
     for (int tb = 0; tb < maxlen; tb += GROUP) {
-      // each lane owns one A entry of the batch: its value and P row bounds
       int t = tb + gl;
       double a = 0.0;
-      int64_t d0 = 0, o0 = 0;
-      int nd = 0, plen = 0;
+      int32_t d0 = 0, o0 = 0;
+      uint32_t pk = 0;  // nd (16 bits) | plen << 16
       if (t < len) {
         int32_t k = __ldg(acol + t0 + t);
         if (NUM) a = __ldg(aval + t0 + t);
-        if (src == 0) {
-          d0 = __ldg(op.pd_rp + k);
-          nd = (int)(__ldg(op.pd_rp + k + 1) - d0);
-          if (op.po_rp) { o0 = __ldg(op.po_rp + k); plen = nd + (int)(__ldg(op.po_rp + k + 1) - o0); }
-          else plen = nd;
-        } else {
-          d0 = __ldg(op.pr_rp + k);
-          nd = plen = (int)(__ldg(op.pr_rp + k + 1) - d0);
+        int64_t x0 = __ldg(qrp + k);
+        d0 = (int32_t)x0;
+        int nd = (int)(__ldg(qrp + k + 1) - x0), plen = nd;
+        if (po_here) {
+          int64_t y0 = __ldg(op.po_rp + k);
+          o0 = (int32_t)y0;
+          plen += (int)(__ldg(op.po_rp + k + 1) - y0);
         }
+        pk = (uint32_t)nd | ((uint32_t)plen << 16);
       }
-      // exclusive scan of the pair counts inside the group
-      int incl = plen;
-#pragma unroll
-      for (int o = 1; o < GROUP; o <<= 1) {
-        int y = __shfl_up_sync(FULL, incl, o, GROUP);
-        if (gl >= o) incl += y;
-      }
-      int excl = incl - plen;
-      int total = __shfl_sync(FULL, incl, GROUP - 1, GROUP);
-      int maxtotal = __reduce_max_sync(FULL, total);
+      int steps = min(GROUP, maxlen - tb);
 #pragma unroll 1
-      for (int w0 = 0; w0 < maxtotal; w0 += WIN) {
-        // expansion: lane writes the descriptors of its pairs inside the window
-        int ub = max(0, w0 - excl), ue = min(plen, w0 + WIN - excl);
-        for (int u = ub; u < ue; ++u) {
-          int q = excl + u - w0;
-          ps.desc[q] = u < nd ? (int32_t)(d0 + u) : (int32_t)((uint32_t)(o0 + (u - nd)) | 0x80000000u);
-          if (NUM) ps.a[q] = a;
+      for (int j = 0; j < steps; ++j) {
+        uint32_t pkj = __shfl_sync(FULL, pk, j, GROUP);
+        int32_t d0j = __shfl_sync(FULL, d0, j, GROUP);
+        double aj = NUM ? __shfl_sync(FULL, a, j, GROUP) : 0.0;
+        int32_t o0j = po_here ? __shfl_sync(FULL, o0, j, GROUP) : 0;
+        int ndj = (int)(pkj & 0xffff), plj = (int)(pkj >> 16);
+        for (int u = gl; u < plj; u += GROUP) {
+          int32_t g;
+          double p = 0.0;
+          if (u < ndj) {
+            g = __ldg(qcol + d0j + u) + coff;
+            if (NUM) p = __ldg(qval + d0j + u);
+          } else {
+            int32_t e = o0j + (u - ndj);
+            g = __ldg(op.p_colmap + __ldg(op.po_col + e));
+            if (NUM) p = __ldg(op.po_val + e);
+          }
+          ok &= table_put<NUM>(keys, vals, log2t, g, NUM ? __dmul_rn(aj, p) : 0.0, nnew);
         }
         __syncwarp();
-        int wtot = min(total - w0, WIN);
-        int rounds = (__reduce_max_sync(FULL, max(wtot, 0)) + GROUP - 1) / GROUP;
-#pragma unroll 1
-        for (int r = 0; r < rounds; ++r) {
-          int q = r * GROUP + gl;
-          bool valid = i >= 0 && q < wtot;
-          int32_t g = 0;
-          double v = 0.0;
-          if (valid) {
-            int32_t e = ps.desc[q];
-            double pv = 0.0;
-            if (e >= 0) { g = __ldg(qcol + e) + coff; if (NUM) pv = __ldg(qval + e); }
-            else {
-              int32_t eo = e & 0x7fffffff;
-              g = __ldg(op.p_colmap + __ldg(op.po_col + eo));
-              if (NUM) pv = __ldg(op.po_val + eo);
-            }
-            if (NUM) v = __dmul_rn(ps.a[q], pv);
-          }
-          unsigned long long key = valid ? (((unsigned long long)gid << 32) | (uint32_t)g)
-                                         : (0xFFFFFFFF00000000ull | (unsigned)lane);
-          unsigned grp = __match_any_sync(FULL, key);
-          bool leader = valid && (__ffs(grp) - 1) == lane;
-          unsigned rest = grp & ~(1u << lane);
-          bool existed = false;
-          int slot = leader ? table_find_or_claim(keys, log2t, g, existed) : 0;
-          if (leader && slot < 0) ok = false;
-          double acc = 0.0;
-          if (NUM && leader && slot >= 0) acc = existed ? __dadd_rn(vals[slot], v) : v;
-          if (NUM) {
-            int steps = __reduce_max_sync(FULL, leader ? __popc(rest) : 0);
-            for (int it = 0; it < steps; ++it) {
-              int srcl = (leader && rest) ? __ffs(rest) - 1 : lane;
-              double x = __shfl_sync(FULL, v, srcl);
-              if (leader && rest) { acc = __dadd_rn(acc, x); rest &= rest - 1; }
-            }
-            if (leader && slot >= 0) vals[slot] = acc;
-          }
-          if (leader && slot >= 0 && !existed) ++nnew;
-          __syncwarp();
-        }
       }
     }
   }
   if (!ok) atomicOr(status, ST_TABLE_FULL);
   return nnew;
+}
+
+// Second walk over row i's pairs in the same fold order as ap_row_accumulate,
+// writing the slot byte of every pair (symbolic map building).  slot_of maps
+// a table position to the key's rank; the first pair of each slot (in fold
+// order) is flagged with 0x80 when flag_first.  `seen` has one int per slot.
+template <int GROUP>
+__device__ __forceinline__ void ap_row_write_smap(const Ops &op, int64_t i, const int32_t *keys, int log2t,
+                                                  const int32_t *slot_of, int32_t *seen, const PStage &ps,
+                                                  uint8_t *smap_row, bool flag_first) {
+  const int gl = threadIdx.x & (GROUP - 1);
+  const bool has_po = op.po_rp != nullptr;
+  int run = 0;
+#pragma unroll 1
+  for (int src = 0; src < 2; ++src) {
+    const int64_t *arp = src ? op.ao_rp : op.ad_rp;
+    if (arp == nullptr) continue;
+    const int32_t *acol = src ? op.ao_col : op.ad_col;
+    const int64_t *qrp = src ? op.pr_rp : op.pd_rp;
+    const int32_t *qcol = src ? op.pr_col : op.pd_col;
+    const int32_t coff = src ? 0 : (int32_t)op.c_lo;
+    const bool po_here = has_po && src == 0;
+    int64_t t0 = 0, t1 = 0;
+    if (i >= 0) { t0 = arp[i]; t1 = arp[i + 1]; }
+    int len = (int)(t1 - t0);
+    int maxlen = __reduce_max_sync(FULL, len);
+#pragma unroll 1
+    for (int tb = 0; tb < maxlen; tb += GROUP) {
+      int t = tb + gl;
+      int32_t d0 = 0, o0 = 0;
+      uint32_t pk = 0;
+      if (t < len) {
+        int32_t k = acol[t0 + t];
+        int64_t x0 = qrp[k];
+        d0 = (int32_t)x0;
+        int nd = (int)(qrp[k + 1] - x0), plen = nd;
+        if (po_here) { o0 = (int32_t)op.po_rp[k]; plen += (int)(op.po_rp[k + 1] - op.po_rp[k]); }
+        pk = (uint32_t)nd | ((uint32_t)plen << 16);
+      }
+      int steps = min(GROUP, maxlen - tb);
+      for (int j = 0; j < steps; ++j) {
+        uint32_t pkj = __shfl_sync(FULL, pk, j, GROUP);
+        int32_t d0j = __shfl_sync(FULL, d0, j, GROUP);
+        int32_t o0j = po_here ? __shfl_sync(FULL, o0, j, GROUP) : 0;
+        int ndj = (int)(pkj & 0xffff), plj = (int)(pkj >> 16);
+        for (int u = gl; u < plj; u += GROUP) {
+          int32_t g = u < ndj ? qcol[d0j + u] + coff : op.p_colmap[op.po_col[o0j + (u - ndj)]];
+          int h = table_find(keys, log2t, g);
+          int sl = h >= 0 ? slot_of[h] : 0;
+          bool first = flag_first && seen[sl] == 0;  // slots of one P row are distinct
+          smap_row[run + u] = (uint8_t)(sl | (first ? 0x80 : 0));
+          seen[sl] = 1;
+        }
+        __syncwarp();
+        run += plj;
+      }
+    }
+  }
 }
 
 // Compact a group's table into (key, value) lists; returns the entry count

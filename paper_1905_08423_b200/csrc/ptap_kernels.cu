@@ -64,17 +64,33 @@ __global__ void k_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_
         if (n <= bin_capacity(q)) { b = q; break; }
     }
   }
+  // block-level aggregation: one global atomic per bin per block
+  __shared__ unsigned scnt[NBINS + 1];
+  __shared__ unsigned long long sbase[NBINS + 1];
   const int lane = lane_id();
+  if (threadIdx.x <= NBINS) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned woff[NBINS];
   unsigned any = __ballot_sync(FULL, b >= 0);
-  if (lane == 0 && any) atomicAdd(selected, (unsigned long long)__popc(any));
+  if (lane == 0 && any) atomicAdd(scnt + NBINS, (unsigned)__popc(any));
+#pragma unroll
   for (int q = 0; q < NBINS; ++q) {
     unsigned bits = __ballot_sync(FULL, b == q);
-    if (!bits) continue;
-    int leader = __ffs(bits) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(bl.count + q, (unsigned long long)__popc(bits));
-    base = __shfl_sync(FULL, base, leader);
-    if (b == q && bl.rows[q]) bl.rows[q][base + __popc(bits & ((1u << lane) - 1u))] = (int32_t)i;
+    unsigned w = 0;
+    if (bits && lane == 0) w = atomicAdd(scnt + q, (unsigned)__popc(bits));
+    woff[q] = __shfl_sync(FULL, w, 0);
+  }
+  __syncthreads();
+  if (threadIdx.x < NBINS) {
+    sbase[threadIdx.x] = scnt[threadIdx.x] ? atomicAdd(bl.count + threadIdx.x, (unsigned long long)scnt[threadIdx.x]) : 0;
+  } else if (threadIdx.x == NBINS && scnt[NBINS]) {
+    atomicAdd(selected, (unsigned long long)scnt[NBINS]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NBINS; ++q) {
+    unsigned bits = __ballot_sync(FULL, b == q);
+    if (b == q && bl.rows[q]) bl.rows[q][sbase[q] + woff[q] + __popc(bits & ((1u << lane) - 1u))] = (int32_t)i;
   }
 }
 
@@ -93,6 +109,7 @@ __global__ void k_max_est(const int32_t *rows, unsigned long long nrows, const i
 struct GroupTables {
   int32_t *keys; double *vals; int32_t *lk;
   PStage ps;
+  int32_t *slot_of; int32_t *sb;  // symbolic only
 };
 // per-group footprint: 8-byte items first (vals[T], a[WIN]) then 4-byte
 // items (keys[T], lk[T/2], desc[WIN]); WIN = PAIRS_PER_LANE * GROUP
@@ -100,7 +117,7 @@ __host__ __device__ inline size_t group_bytes(int log2t, bool num, int group) {
   size_t T = (size_t)1 << log2t;
   size_t W = (size_t)PAIRS_PER_LANE * group;
   size_t b8 = num ? (T + W) * 8 : 0;
-  size_t b4 = T * 4 + (T / 2) * 4 + W * 4;
+  size_t b4 = T * 4 + (T / 2) * 4 + W * 4 + (num ? 0 : T * 4 + (T / 2) * 4);  // symbolic: slot_of[T], sb[T/2]
   return (b8 + b4 + 15) & ~(size_t)15;
 }
 template <int GROUP, bool NUM, bool GT>
@@ -123,7 +140,9 @@ __device__ __forceinline__ GroupTables group_tables(unsigned char *gtables, int 
   }
   t.keys = (int32_t *)q; q += (size_t)T * 4;
   t.lk = (int32_t *)q; q += (size_t)(T / 2) * 4;
-  t.ps.desc = (int32_t *)q;
+  t.ps.desc = (int32_t *)q; q += (size_t)W * 4;
+  t.slot_of = NUM ? nullptr : (int32_t *)q; q += NUM ? 0 : (size_t)T * 4;
+  t.sb = NUM ? nullptr : (int32_t *)q;
   return t;
 }
 
@@ -173,13 +192,15 @@ __device__ __forceinline__ void arena_insert(unsigned long long *ar, unsigned lo
 template <int GROUP, bool GT>
 __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *rows, unsigned long long nrows,
                                                         int log2t, unsigned char *gtables, int do_send,
-                                                        int do_local, Arena local, Arena send, int *status) {
+                                                        int do_local, Arena local, Arena send, MapOut mo,
+                                                        int *status) {
   GroupTables tb = group_tables<GROUP, false, GT>(gtables, log2t);
   const int gpw = 32 / GROUP;
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
   const int gl = lane_id() & (GROUP - 1);
   const unsigned long long m = (unsigned long long)op.m;
+  const bool maps = mo.smap != nullptr;
   for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
        r0 += (unsigned long long)gridDim.x * gpc) {
     unsigned long long ridx = r0 + lane_id() / GROUP;
@@ -194,6 +215,40 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
     table_clear<GROUP>(tb.keys, T);
     ap_row_accumulate<GROUP, false>(op, i, tb.keys, nullptr, log2t, tb.ps, status);
     int n = table_compact<GROUP, false>(tb.keys, nullptr, T, tb.lk, nullptr);
+    if (maps) {
+      // sorted pattern of the row (slot = rank), then the slot map of its pairs
+      int P2 = 1;
+      while (P2 < n) P2 <<= 1;
+      int maxP2 = __reduce_max_sync(FULL, i >= 0 ? P2 : 1);
+      for (int x = gl; x < maxP2; x += GROUP) tb.sb[x] = (i >= 0 && x < n) ? tb.lk[x] : INT32_MAX;
+      __syncwarp();
+      for (int k = 2; k <= maxP2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int x = gl; x < maxP2; x += GROUP) {
+            int y = x ^ j;
+            if (y > x) {
+              bool up = (x & k) == 0;
+              int32_t kx = tb.sb[x], ky = tb.sb[y];
+              if ((kx > ky) == up) { tb.sb[x] = ky; tb.sb[y] = kx; }
+            }
+          }
+          __syncwarp();
+        }
+      if (i >= 0) {
+        int32_t *pat = mo.pat + mo.pat_rp[i];
+        for (int x = gl; x < n; x += GROUP) {
+          int32_t g = tb.sb[x];
+          pat[x] = g;
+          tb.slot_of[table_find(tb.keys, log2t, g)] = x;
+        }
+        if (gl == 0) mo.nap[i] = (uint8_t)n;
+      }
+      __syncwarp();
+      for (int x = gl; x < maxP2; x += GROUP) tb.sb[x] = 0;  // seen[slot]
+      __syncwarp();
+      ap_row_write_smap<GROUP>(op, i, tb.keys, log2t, tb.slot_of, tb.sb, tb.ps,
+                               mo.smap + (i >= 0 ? mo.smap_rp[i] : 0), n <= 127);
+    }
     if (i >= 0 && n > 0) {
       if (wl) {
         int tot = (int)(pd1 - pd0) * n;
@@ -213,6 +268,50 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
       }
     }
     __syncwarp();
+  }
+}
+
+// Position maps: for every target row J of P(i,:) (local C row or staging
+// row), the position of each AP slot of row i inside row J, found by a
+// binary search of the row's sorted pattern.  8-lane groups, 4 rows per warp.
+__global__ void __launch_bounds__(256) k_build_pmap(Ops op, unsigned long long nrows, MapArgs mp, MapOut mo,
+                                                    OuterTargets tg, int *status) {
+  constexpr int G = 8;
+  const int gl = lane_id() & (G - 1);
+  const int gpc = (blockDim.x >> 5) * (32 / G);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * (32 / G); r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / G;
+    if (ridx >= nrows) continue;
+    int64_t i = (int64_t)ridx;
+    int64_t pd0 = op.pd_rp[i], pd1 = op.pd_rp[i + 1], po0 = 0, po1 = 0;
+    if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
+    int ndP = (int)(pd1 - pd0), nP = ndP + (int)(po1 - po0);
+    if (nP == 0) continue;
+    int n = mp.nap[i];
+    const int32_t *pat = mo.pat + mo.pat_rp[i];
+    uint8_t *pm = mp.pmap + mp.pmap_rp[i];
+    for (int jj = 0; jj < nP; ++jj) {
+      int64_t c0, c1;
+      const int32_t *ccol;
+      if (jj < ndP) {
+        int32_t J = op.pd_col[pd0 + jj];
+        c0 = tg.c_rp[J]; c1 = tg.c_rp[J + 1]; ccol = tg.c_col;
+      } else {
+        int32_t sr = mp.po_srow[po0 + (jj - ndP)];
+        if (sr < 0) { if (gl == 0) atomicOr(status, ST_DRIFT); continue; }
+        c0 = tg.s_rp[sr]; c1 = tg.s_rp[sr + 1]; ccol = tg.s_col;
+      }
+      for (int64_t e = c0 + gl; e < c1; e += G) {
+        int32_t g = ccol[e];
+        int lo = 0, hi = n;
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (pat[mid] < g) lo = mid + 1; else hi = mid;
+        }
+        if (lo < n && pat[lo] == g) pm[(int64_t)jj * n + lo] = (uint8_t)(e - c0);
+      }
+    }
   }
 }
 
@@ -791,13 +890,13 @@ cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *
 }
 
 cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
-                                  int do_send, int do_local, Arena local, Arena send, int *status,
+                                  int do_send, int do_local, Arena local, Arena send, const MapOut &mo, int *status,
                                   cudaStream_t stream) {
   const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
   unsigned char *gtables = s.gtables;
   cudaError_t e;
   PTAP_ROWKERNEL_DISPATCH(k_outer_symbolic, false, op, rows, nrows, log2t, gtables, do_send, do_local, local, send,
-                          status);
+                          mo, status);
 }
 
 cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
@@ -1022,6 +1121,15 @@ cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t tar
                            cudaStream_t st) {
   if (nrows > 0)
     k_ptc_est<<<nblk(nrows, 256), 256, 0, st>>>(nrows, target_map, target_offset, is_staging, t_nrows, t_rows, t_rp, est);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const MapArgs &mp, const MapOut &mo,
+                              const OuterTargets &tg, int *status, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  unsigned long long grid = (nrows + 31) / 32;
+  if (grid > 148ull * 64) grid = 148ull * 64;
+  k_build_pmap<<<(int)grid, 256, 0, st>>>(op, nrows, mp, mo, tg, status);
   return cudaGetLastError();
 }
 

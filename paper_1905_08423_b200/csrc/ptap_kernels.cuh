@@ -9,11 +9,11 @@ namespace ptapdev {
 
 // Work bins: estimated distinct AP-row keys n -> table shape.
 //   bin 0: n <= 32    4 rows per warp (8-lane groups), 64-slot shared tables
-//   bin 1: n <= 256   1 row per warp, 512-slot shared tables
-//   bin 2: n <= 2048  1 row per warp, 4096-slot shared tables
+//   bin 1: n <= 128   4 rows per warp, 256-slot shared tables
+//   bin 2: n <= 1024  1 row per warp, 2048-slot shared tables
 //   bin 3: larger     1 row per warp, global-memory tables (heavy rows)
 constexpr int NBINS = 4;
-__host__ __device__ inline int64_t bin_capacity(int q) { return q == 0 ? 32 : (q == 1 ? 256 : 2048); }
+__host__ __device__ inline int64_t bin_capacity(int q) { return q == 0 ? 32 : (q == 1 ? 128 : 1024); }
 
 struct BinLists {
   int32_t *rows[NBINS];
@@ -40,6 +40,14 @@ struct PtcTarget {
 };
 
 // plan-mapped numeric (ptap_mapped.cu)
+struct MapOut {  // symbolic outputs of the outer-product pass (null: no maps)
+  const int64_t *smap_rp;
+  uint8_t *smap;
+  uint8_t *nap;
+  const int64_t *pat_rp;  // sorted AP row patterns (transient, for the position maps)
+  int32_t *pat;
+};
+
 struct MapArgs {
   int64_t *smap_rp;  // [nloc+1] offsets into smap
   uint8_t *smap;     // slot of every (A entry, P entry) pair, fold order
@@ -67,8 +75,10 @@ cudaError_t launch_max_est(const int32_t *rows, unsigned long long nrows, const 
 cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                             int64_t *ap_nnz, int *status, cudaStream_t stream);
 cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
-                                  int do_send, int do_local, Arena local, Arena send, int *status,
+                                  int do_send, int do_local, Arena local, Arena send, const MapOut &mo, int *status,
                                   cudaStream_t stream);
+cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const MapArgs &mp, const MapOut &mo,
+                              const OuterTargets &tg, int *status, cudaStream_t st);
 cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                  int do_send, int do_local, const OuterTargets &tg, int *status,
                                  cudaStream_t stream);
@@ -124,8 +134,7 @@ cudaError_t launch_po_srow(int64_t nnz, const int32_t *po_col, const int32_t *co
                            const int32_t *s_rows, int32_t *po_srow, int *status, cudaStream_t st);
 cudaError_t launch_max_i64(int64_t n, const int64_t *v, unsigned long long *mx, cudaStream_t st);
 cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *mx, cudaStream_t st);
-cudaError_t launch_build_maps(const Ops &op, const int32_t *rows, unsigned long long nrows, const MapArgs &mp,
-                              const OuterTargets &tg, int *status, cudaStream_t st);
+
 cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                         const MapArgs &mp, const OuterTargets &tg, int do_send, int do_local,
                                         int *status, cudaStream_t st);

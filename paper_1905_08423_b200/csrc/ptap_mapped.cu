@@ -1,7 +1,7 @@
 // ptap_mapped.cu -- plan-mapped numeric pass of the all-at-once / merged
 // triple product.
 //
-// The symbolic phase (k_build_maps) records, for every fine row i it will
+// The symbolic phase (k_outer_symbolic + k_build_pmap) records, for every fine row i it will
 // process, two byte maps that make the numeric pass free of hashing and of
 // searches in C -- the "caching intermediate data" mode of the paper
 // (Table 6) applied to the outer-product algorithm:
@@ -69,125 +69,6 @@ __global__ void k_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *m
   if (lane_id() == 0 && x) atomicMax(mx, x);
 }
 
-// ---------------------------------------------------------------------------
-// map builder: one warp per row (symbolic only)
-// ---------------------------------------------------------------------------
-constexpr int MAP_LOG2T = 9;  // 512-slot tables: up to 255 AP columns
-constexpr int MAP_T = 1 << MAP_LOG2T;
-
-__global__ void __launch_bounds__(256) k_build_maps(Ops op, const int32_t *rows, unsigned long long nrows,
-                                                    MapArgs mp, OuterTargets tg, int *status) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int wpc = blockDim.x >> 5;
-  // per warp: keys[T], lk[T/2], desc[256], slot_of[T], sortbuf[256]
-  unsigned char *base = smem + (size_t)warp * (MAP_T * 4 + (MAP_T / 2) * 4 + 256 * 4 + MAP_T * 4 + 256 * 4);
-  int32_t *keys = (int32_t *)base;
-  int32_t *lk = keys + MAP_T;
-  PStage ps;
-  ps.desc = lk + MAP_T / 2;
-  ps.a = nullptr;
-  int32_t *slot_of = ps.desc + 256;
-  int32_t *sb = slot_of + MAP_T;
-  for (unsigned long long r = (unsigned long long)blockIdx.x * wpc + warp; r < nrows;
-       r += (unsigned long long)gridDim.x * wpc) {
-    int64_t i = rows ? (int64_t)rows[r] : (int64_t)r;
-    int64_t pd0 = op.pd_rp[i], pd1 = op.pd_rp[i + 1], po0 = 0, po1 = 0;
-    if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
-    int ndP = (int)(pd1 - pd0), nP = ndP + (int)(po1 - po0);
-    if (nP == 0) continue;  // warp-uniform (one row per warp)
-    table_clear<32>(keys, MAP_T);
-    ap_row_accumulate<32, false>(op, i, keys, nullptr, MAP_LOG2T, ps, status);
-    int n = table_compact<32, false>(keys, nullptr, MAP_T, lk, nullptr);
-    if (n > 255) {
-      if (lane == 0) atomicOr(status, ST_TABLE_FULL);
-      continue;
-    }
-    // sort the row's columns: slot = rank
-    int P2 = 1;
-    while (P2 < n) P2 <<= 1;
-    for (int x = lane; x < P2; x += 32) sb[x] = x < n ? lk[x] : INT32_MAX;
-    __syncwarp();
-    for (int k = 2; k <= P2; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int x = lane; x < P2; x += 32) {
-          int y = x ^ j;
-          if (y > x) {
-            bool up = (x & k) == 0;
-            int32_t kx = sb[x], ky = sb[y];
-            if ((kx > ky) == up) { sb[x] = ky; sb[y] = kx; }
-          }
-        }
-        __syncwarp();
-      }
-    for (int x = lane; x < n; x += 32) slot_of[table_find(keys, MAP_LOG2T, sb[x])] = x;
-    __syncwarp();
-    if (lane == 0) mp.nap[i] = (uint8_t)n;
-    // smap: pairs in fold order; the first pair of every slot carries 0x80
-    // ("set" instead of "add": the reference's hm_add semantics, and no
-    // zero-fill of the accumulator) when the slot fits in 7 bits
-    const bool flag_first = n <= 127;
-    for (int x = lane; x < n; x += 32) sb[x] = 0;  // seen[slot]
-    __syncwarp();
-    int64_t run = mp.smap_rp[i];
-    for (int src = 0; src < 2; ++src) {
-      const int64_t *arp = src ? op.ao_rp : op.ad_rp;
-      if (!arp) continue;
-      const int32_t *acol = src ? op.ao_col : op.ad_col;
-      for (int64_t t = arp[i]; t < arp[i + 1]; ++t) {
-        int32_t k = acol[t];
-        int64_t d0, d1, o0 = 0, o1 = 0;
-        if (src == 0) {
-          d0 = op.pd_rp[k]; d1 = op.pd_rp[k + 1];
-          if (op.po_rp) { o0 = op.po_rp[k]; o1 = op.po_rp[k + 1]; }
-        } else {
-          d0 = op.pr_rp[k]; d1 = op.pr_rp[k + 1];
-        }
-        int nd = (int)(d1 - d0), plen = nd + (int)(o1 - o0);
-        for (int u = lane; u < plen; u += 32) {
-          int32_t g;
-          if (u < nd) g = src ? op.pr_col[d0 + u] : op.pd_col[d0 + u] + (int32_t)op.c_lo;
-          else g = op.p_colmap[op.po_col[o0 + (u - nd)]];
-          int h = table_find(keys, MAP_LOG2T, g);
-          int sl = h >= 0 ? slot_of[h] : 0;
-          int first = (flag_first && sb[sl] == 0) ? 0x80 : 0;
-          mp.smap[run + u] = (uint8_t)(sl | first);
-          if (h < 0) atomicOr(status, ST_DRIFT);
-        }
-        __syncwarp();
-        for (int u = lane; u < plen; u += 32) sb[mp.smap[run + u] & 0x7f] = 1;
-        __syncwarp();
-        run += plen;
-      }
-    }
-    // pmap: every target row of P(i,:)
-    int64_t pb = mp.pmap_rp[i];
-    for (int jj = 0; jj < nP; ++jj) {
-      int64_t c0, c1;
-      const int32_t *ccol;
-      if (jj < ndP) {
-        int32_t J = op.pd_col[pd0 + jj];
-        c0 = tg.c_rp[J]; c1 = tg.c_rp[J + 1]; ccol = tg.c_col;
-      } else {
-        int32_t sr = mp.po_srow[po0 + (jj - ndP)];
-        if (sr < 0) { if (lane == 0) atomicOr(status, ST_DRIFT); continue; }
-        c0 = tg.s_rp[sr]; c1 = tg.s_rp[sr + 1]; ccol = tg.s_col;
-      }
-      int found = 0;
-      for (int64_t e = c0 + lane; e < c1; e += 32) {
-        int h = table_find(keys, MAP_LOG2T, ccol[e]);
-        if (h >= 0) { mp.pmap[pb + (int64_t)jj * n + slot_of[h]] = (uint8_t)(e - c0); ++found; }
-      }
-      for (int o = 16; o > 0; o >>= 1) found += __shfl_xor_sync(FULL, found, o);
-      if (found != n && lane == 0) atomicOr(status, ST_DRIFT);
-    }
-    __syncwarp();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// numeric: G lanes per row; 32/G rows per warp
-// ---------------------------------------------------------------------------
 struct __align__(16) StepEntry {
   double a;        // A value of the entry
   int32_t d0;      // start of its P_d (or remote) row
@@ -372,19 +253,6 @@ cudaError_t launch_max_i64(int64_t n, const int64_t *v, unsigned long long *mx, 
 
 cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *mx, cudaStream_t st) {
   if (n > 0) k_max_rowlen<<<nb(n, 256), 256, 0, st>>>(n, rp, mx);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_build_maps(const Ops &op, const int32_t *rows, unsigned long long nrows, const MapArgs &mp,
-                              const OuterTargets &tg, int *status, cudaStream_t st) {
-  if (nrows == 0) return cudaSuccess;
-  const int warps = 4;
-  size_t sm = (size_t)warps * (MAP_T * 4 + (MAP_T / 2) * 4 + 256 * 4 + MAP_T * 4 + 256 * 4);
-  cudaError_t e = opt_in(k_build_maps, sm);
-  if (e != cudaSuccess) return e;
-  unsigned long long grid = (nrows + warps - 1) / warps;
-  if (grid > 148ull * 64) grid = 148ull * 64;
-  k_build_maps<<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, status);
   return cudaGetLastError();
 }
 
