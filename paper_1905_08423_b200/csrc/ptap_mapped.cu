@@ -25,7 +25,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ptap_device.cuh"
 #include "ptap_kernels.cuh"
@@ -214,6 +216,22 @@ __global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int3
   }
 }
 
+// Grid size of the grid-stride numeric kernels: PTAP_GRID_RESIDENT=1 caps the
+// grid at the resident CTA count (one contiguous band of rows in flight);
+// the default oversubscribes the grid (148 x 64 CTAs).
+template <typename K>
+static unsigned long long grid_cap(K kern, int threads, size_t smem) {
+  static int mode = -1;
+  if (mode < 0) mode = getenv("PTAP_GRID_RESIDENT") ? 1 : 0;
+  if (!mode) return 148ull * 64;
+  int dev = 0, nsm = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return (unsigned long long)nsm * per_sm;
+}
+
 template <typename K>
 static cudaError_t opt_in(K kern, size_t bytes) {
   if (bytes > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -268,7 +286,7 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
     size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
-    if (grid > 148ull * 64) grid = 148ull * 64;
+    grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
     k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
                                                                     status);
   } else {
@@ -277,7 +295,7 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
     size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
-    if (grid > 148ull * 64) grid = 148ull * 64;
+    grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
     k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
                                                                     status);
   }
