@@ -77,8 +77,11 @@ struct __align__(16) StepEntry {
   uint32_t pk;     // pair offset (16 bits) | nd (8 bits) << 16 | plen (8 bits) << 24
 };
 
+#ifndef PTAP_MINB
+#define PTAP_MINB 1
+#endif
 template <int G, int NAPCAP>
-__global__ void __launch_bounds__(256) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
+__global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
                                                               MapArgs mp, OuterTargets tg, int do_send, int do_local,
                                                               int *status) {
   extern __shared__ __align__(16) unsigned char smem[];
