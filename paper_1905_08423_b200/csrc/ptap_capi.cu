@@ -1071,7 +1071,11 @@ ptap_status ptap_spgemm_ap_numeric(const ptap_operands *ops, const int64_t *row_
 }
 
 ptap_status ptap_device_free(void *ptr, void *stream) {
-  if (ptr) cudaFreeAsync(ptr, (cudaStream_t)stream);
+  // buffers handed out by ptap_spgemm_ap_symbolic come from cudaMalloc
+  if (ptr) {
+    cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(ptr);
+  }
   return PTAP_OK;
 }
 
