@@ -92,7 +92,7 @@ struct ptap_plan {
   int64_t cur[5] = {0, 0, 0, 0, 0}, peak[5] = {0, 0, 0, 0, 0};
   int64_t prod_cur = 0, prod_peak = 0, total_cur = 0, total_peak = 0;
   int *d_status = nullptr;
-  unsigned long long *d_u64 = nullptr;  // 16 scratch counters
+  unsigned long long *d_u64 = nullptr;  // 24 scratch counters
   bool released = false;
   bool symbolic_done = false;
   BinSet bins_send, bins_local, bins_all, bins_ptd, bins_pto;
@@ -640,7 +640,7 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
   p->ncl = ops->c_hi - ops->c_lo;
   p->colmap_len = ops->p_colmap_len;
   cudaError_t e = cudaMalloc(&p->d_status, sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_u64, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_u64, 24 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(p->d_status, 0, sizeof(int));
   if (e != cudaSuccess) {
     delete p;

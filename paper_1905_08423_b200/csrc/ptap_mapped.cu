@@ -77,11 +77,95 @@ struct __align__(16) StepEntry {
   uint32_t pk;     // pair offset (16 bits) | nd (8 bits) << 16 | plen (8 bits) << 24
 };
 
+// resident CTAs per SM requested from ptxas: the kernel is bound by load
+// latency, so the 4-lane instantiation trades a few spilled registers for
+// 48 resident warps (measured: 6 -> 8.55 ms, 5 -> 8.66 ms, 7 -> 9.57 ms)
 #ifndef PTAP_MINB
-#define PTAP_MINB 1
+#define PTAP_MINB 6
 #endif
+#ifndef PTAP_PF
+#define PTAP_PF 1
+#endif
+#ifndef PTAP_OUTER_SERIAL
+#define PTAP_OUTER_SERIAL 0
+#endif
+// Outer-product phase shared by the mapped kernels: the target rows of
+// P(i,:) are fetched G at a time (lane gl of the group loads target jb+gl:
+// column, value and row start) so the dependent loads of all targets are in
+// flight together; the group then walks them in order, lane gl scattering
+// slots gl, gl+G, ... of AP(i,:) with fp64 atomics.
+template <int G, int NREG>
+__device__ __forceinline__ void outer_scatter(const Ops &op, const MapArgs &mp, const OuterTargets &tg, int64_t i,
+                                              int64_t pd0, int64_t pd1, int64_t po0, int64_t po1, bool wl, bool ws,
+                                              int nap, const double (&accr)[NREG], int gl) {
+  const int ndP = (int)(pd1 - pd0);
+  const int nP = ndP + (int)(po1 - po0);
+  const int maxj = __reduce_max_sync(FULL, i >= 0 ? nP : 0);
+  const int64_t pbase = i >= 0 ? __ldg(mp.pmap_rp + i) : 0;
+#if PTAP_OUTER_SERIAL
+  for (int jj = 0; jj < maxj; ++jj) {
+    bool live = i >= 0 && jj < nP && (jj < ndP ? wl : ws);
+    if (live) {
+      double pij;
+      int64_t base;
+      double *cval;
+      if (jj < ndP) {
+        int32_t J = __ldg(op.pd_col + pd0 + jj);
+        pij = __ldg(op.pd_val + pd0 + jj);
+        base = __ldg(tg.c_rp + J);
+        cval = tg.c_val;
+      } else {
+        int64_t e = po0 + (jj - ndP);
+        pij = __ldg(op.po_val + e);
+        base = __ldg(tg.s_rp + __ldg(mp.po_srow + e));
+        cval = tg.s_val;
+      }
+      const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
+#pragma unroll
+      for (int k = 0; k < NREG; ++k) {
+        int s = gl + G * k;
+        if (s < nap) atomicAdd(cval + base + __ldg(pm + s), __dmul_rn(pij, accr[k]));
+      }
+    }
+  }
+  return;
+#endif
+  for (int jb = 0; jb < maxj; jb += G) {
+    const int jm = jb + gl;
+    double pij = 0.0;
+    int64_t base = -1;  // -1: nothing to scatter for this target
+    if (i >= 0 && jm < nP) {
+      if (jm < ndP) {
+        if (wl) {
+          int32_t J = __ldg(op.pd_col + pd0 + jm);
+          pij = __ldg(op.pd_val + pd0 + jm);
+          base = __ldg(tg.c_rp + J);
+        }
+      } else if (ws) {
+        int64_t e = po0 + (jm - ndP);
+        pij = __ldg(op.po_val + e);
+        base = __ldg(tg.s_rp + __ldg(mp.po_srow + e));
+      }
+    }
+    const int cnt = min(G, maxj - jb);
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t b = __shfl_sync(FULL, base, q, G);
+      const double pv = __shfl_sync(FULL, pij, q, G);
+      if (b >= 0) {
+        double *cval = (jb + q < ndP) ? tg.c_val : tg.s_val;
+        const uint8_t *pm = mp.pmap + pbase + (int64_t)(jb + q) * nap;
+#pragma unroll
+        for (int k = 0; k < NREG; ++k) {
+          int s = gl + G * k;
+          if (s < nap) atomicAdd(cval + b + __ldg(pm + s), __dmul_rn(pv, accr[k]));
+        }
+      }
+    }
+  }
+}
+
 template <int G, int NAPCAP>
-__global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
+__global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
                                                               MapArgs mp, OuterTargets tg, int do_send, int do_local,
                                                               int *status) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -160,6 +244,47 @@ __global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_mapped(Ops op,
         int ctot = __shfl_sync(FULL, incl, G - 1, G);
         __syncwarp();
         int steps = min(G, maxlen - tb);
+#if PTAP_PF
+        if constexpr (G <= 8) {
+          // the P values and slots of all G steps are loaded before the
+          // folds (independent loads in flight together); the folds stay in
+          // step order
+          double pv[G];
+          int sv[G];
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            pv[j] = 0.0; sv[j] = 0;
+            if (j < steps) {
+              const StepEntry ej = ent[j];
+              const int plj = (int)(ej.pk >> 24), ndj = (int)((ej.pk >> 16) & 0xff);
+              if (gl < plj) {
+                pv[j] = gl < ndj ? __ldg(qval + ej.d0 + gl) : __ldg(op.po_val + ent_o0[j] + (gl - ndj));
+                sv[j] = __ldg(smap + (ej.pk & 0xffff) + gl);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            if (j < steps) {
+              const StepEntry ej = ent[j];
+              const int plj = (int)(ej.pk >> 24);
+              if (gl < plj) {
+                int s = sv[j], sl = (nap > 127) ? s : (s & 0x7f);
+                double prod = __dmul_rn(ej.a, pv[j]);
+                acc[sl] = (nap <= 127 && (s & 0x80)) ? prod : __dadd_rn(acc[sl], prod);
+                const int ndj = (int)((ej.pk >> 16) & 0xff);
+                for (int u = gl + G; u < plj; u += G) {
+                  double p = u < ndj ? __ldg(qval + ej.d0 + u) : __ldg(op.po_val + ent_o0[j] + (u - ndj));
+                  int s2 = __ldg(smap + (ej.pk & 0xffff) + u), sl2 = (nap > 127) ? s2 : (s2 & 0x7f);
+                  double pr2 = __dmul_rn(ej.a, p);
+                  acc[sl2] = (nap <= 127 && (s2 & 0x80)) ? pr2 : __dadd_rn(acc[sl2], pr2);
+                }
+              }
+              __syncwarp();
+            }
+          }
+        } else
+#endif
 #pragma unroll 1
         for (int j = 0; j < steps; ++j) {
           const StepEntry ej = ent[j];  // one 16-byte shared load per step
@@ -186,35 +311,7 @@ __global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_mapped(Ops op,
 #pragma unroll
     for (int r = 0; r < NREG; ++r) accr[r] = (gl + G * r < nap) ? acc[gl + G * r] : 0.0;
     // outer products into C (local rows) and the staging (send rows)
-    int ndP = (int)(pd1 - pd0);
-    int nP = ndP + (int)(po1 - po0);
-    int maxj = __reduce_max_sync(FULL, i >= 0 ? nP : 0);
-    int64_t pbase = i >= 0 ? __ldg(mp.pmap_rp + i) : 0;
-    for (int jj = 0; jj < maxj; ++jj) {
-      bool live = i >= 0 && jj < nP && (jj < ndP ? wl : ws);
-      if (live) {
-        double pij;
-        int64_t base;
-        double *cval;
-        if (jj < ndP) {
-          int32_t J = __ldg(op.pd_col + pd0 + jj);
-          pij = __ldg(op.pd_val + pd0 + jj);
-          base = __ldg(tg.c_rp + J);
-          cval = tg.c_val;
-        } else {
-          int64_t e = po0 + (jj - ndP);
-          pij = __ldg(op.po_val + e);
-          base = __ldg(tg.s_rp + __ldg(mp.po_srow + e));
-          cval = tg.s_val;
-        }
-        const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
-#pragma unroll
-        for (int r = 0; r < NREG; ++r) {
-          int s = gl + G * r;
-          if (s < nap) atomicAdd(cval + base + __ldg(pm + s), __dmul_rn(pij, accr[r]));
-        }
-      }
-    }
+    outer_scatter<G, NREG>(op, mp, tg, i, pd0, pd1, po0, po1, wl, ws, nap, accr, gl);
     __syncwarp();
   }
 }
