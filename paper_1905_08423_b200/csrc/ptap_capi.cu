@@ -10,6 +10,7 @@
 //   plan_cache           bin row lists, all-at-once staging, received-slot map, transpose permutations
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -102,6 +103,7 @@ struct ptap_plan {
   Arena local_arena{nullptr, 0};
   // plan-mapped numeric (all-at-once / merged)
   bool mapped = false;
+  bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
   bool want_maps = false;
   MapArgs maps{};
   MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
@@ -492,7 +494,7 @@ ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
 // computed once here so numeric passes do no hashing and no searching.
 // Plan-mapped numeric, part 1 (before the outer-product symbolic pass): the
 // slot maps are written by that pass itself, so allocate them here.
-ptap_status prepare_maps(ptap_plan *p, const Ops &op, cudaStream_t st) {
+ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
   p->want_maps = false;
   if (getenv("PTAP_NO_MAPS")) return PTAP_OK;
   unsigned long long *mx = p->d_u64 + 12;
@@ -505,6 +507,14 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, cudaStream_t st) {
   CK(cudaStreamSynchronize(st));
   p->cnt.kernel_launches += 3;
   if (h[0] > 255 || h[1] > 65535 || h[2] > 255) return PTAP_OK;  // hash path for this plan
+  {
+    // bin 0 through k_outer_numeric_q4: <= 128 map bytes per row and every
+    // offset it touches within 32 bits
+    const int64_t lim = INT32_MAX;
+    const int64_t nnz_max = std::max<int64_t>({ops->a_diag.nnz, ops->a_off.nnz, ops->p_diag.nnz, ops->p_off.nnz,
+                                      ops->p_remote.nnz});
+    p->q4 = h[1] <= 128 && p->nloc < lim && nnz_max < lim && !getenv("PTAP_NO_Q4");
+  }
   int64_t *slen = nullptr, *scratch = nullptr;
   CKS(palloc(p, &slen, p->nloc, CAT_TRANSIENT, st));
   CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
@@ -523,7 +533,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, cudaStream_t st) {
   pfree(p, unused, st);
   pfree(p, scratch, st);
   p->smap_bytes = tot[0];
-  CKS(palloc(p, &p->maps.smap, tot[0], CAT_PLAN, st));
+  CKS(palloc(p, &p->maps.smap, tot[0] + 16, CAT_PLAN, st));  // padded: staged word-wise
   CKS(palloc(p, &p->maps.nap, p->nloc, CAT_PLAN, st));
   CKS(palloc(p, &p->pat, tot[1], CAT_TRANSIENT, st));
   p->mo = MapOut{p->maps.smap_rp, p->maps.smap, p->maps.nap, p->pat_rp, p->pat};
@@ -595,7 +605,7 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
     for (int q = 0; q < NBINS; ++q) {
       if (bs.count[q] == 0) continue;
       const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
-      CK(launch_outer_numeric_mapped(q == 0 ? 0 : 1, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
+      CK(launch_outer_numeric_mapped(q == 0 ? (p->q4 ? 3 : 0) : 1, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
                                      do_local, p->d_status, st));
       p->cnt.kernel_launches++;
     }
@@ -669,7 +679,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   Tracer tr;
   CKS(ap_sizes(p, op, &p->ap_nnz, st, &p->apub));
   tr.mark(st, "ap_sizes");
-  if (p->alg != PTAP_TWO_STEP) CKS(prepare_maps(p, op, st));
+  if (p->alg != PTAP_TWO_STEP) CKS(prepare_maps(p, op, ops, st));
   tr.mark(st, "prepare_maps");
   if (p->alg == PTAP_TWO_STEP) {
     // C~ = A P (src/spgemm.py:184-202), booked as auxiliary

@@ -89,6 +89,22 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_OUTER_SERIAL
 #define PTAP_OUTER_SERIAL 0
 #endif
+#ifndef PTAP_GPAD
+#define PTAP_GPAD 0
+#endif
+#ifndef PTAP_AOFF
+#define PTAP_AOFF 0
+#endif
+// per-group shared region: accumulator (NAPCAP + 1 slots, optionally shifted
+// by PTAP_AOFF bytes), then G step entries and G P_o row starts; PTAP_GPAD
+// pads the region to move successive groups to other shared-memory banks
+__host__ __device__ constexpr size_t acc_region_bytes(int napcap) {
+  return (((size_t)(napcap + 1) * 8 + PTAP_AOFF + 15) & ~(size_t)15);
+}
+__host__ __device__ constexpr size_t group_bytes(int g, int napcap) {
+  return ((acc_region_bytes(napcap) + (size_t)g * 16 + (size_t)g * 4 + 15) & ~(size_t)15) + PTAP_GPAD;
+}
+
 // Outer-product phase shared by the mapped kernels: the target rows of
 // P(i,:) are fetched G at a time (lane gl of the group loads target jb+gl:
 // column, value and row start) so the dependent loads of all targets are in
@@ -175,10 +191,10 @@ __global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_m
   const int gpc = (blockDim.x >> 5) * gpw;
   const int gid = (threadIdx.x >> 5) * gpw + lane / G;
   // per group: acc[NAPCAP + 1] (f64, +1 pad spreads groups over banks), ent[G], o0[G]
-  const size_t gbytes = ((((size_t)(NAPCAP + 1) * 8 + 15) & ~(size_t)15) + G * sizeof(StepEntry) + G * 4 + 15) & ~(size_t)15;
+  constexpr size_t gbytes = group_bytes(G, NAPCAP);
   unsigned char *gbase = smem + (size_t)gid * gbytes;
-  double *acc = (double *)gbase;
-  StepEntry *ent = (StepEntry *)(gbase + (((size_t)(NAPCAP + 1) * 8 + 15) & ~(size_t)15));
+  double *acc = (double *)(gbase + PTAP_AOFF);
+  StepEntry *ent = (StepEntry *)(gbase + acc_region_bytes(NAPCAP));
   int32_t *ent_o0 = (int32_t *)(ent + G);
   const bool has_po = op.po_rp != nullptr;
   for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
@@ -316,6 +332,173 @@ __global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_m
   }
 }
 
+// Bin-0 kernel (AP rows of at most 32 slots): 8 fine rows per warp, 4 lanes
+// per row.  Same fold order, rounding and scatter as k_outer_numeric_mapped,
+// with the shared-memory traffic cut down (the kernel is bound by the L1
+// data pipe): the slot maps of a batch of consecutive rows are copied into
+// shared memory with one coalesced sweep instead of 8 row-strided byte
+// gathers per step, and the step entries live in [step][row] arrays so each
+// per-step broadcast is a single conflict-free 8-byte load.
+constexpr int Q4_RPW = 8, Q4_G = 4, Q4_CAP = 32, Q4_ACC = 36, Q4_SMW = 264;
+struct __align__(16) Q4Warp {
+  double a[Q4_G][Q4_RPW];     // A value of step j, row r
+  int2 dp[Q4_G][Q4_RPW];      // start of its P row, packed offsets/lengths
+  int32_t o0[Q4_G][Q4_RPW];   // start of its P_o row
+  uint32_t sm[Q4_SMW];        // slot maps of the batch
+};
+static inline size_t q4_smem(int warps) {
+  return (size_t)warps * (Q4_RPW * Q4_ACC * sizeof(double) + sizeof(Q4Warp));
+}
+
+// fold of one A block (SRC 0: A_d with P_d/P_o rows, 1: A_o with the
+// gathered remote rows) for the 8 rows of a q4 batch; a template so that the
+// block's arrays are kernel parameters, not registers
+template <int SRC>
+__device__ __forceinline__ void q4_fold(const Ops &op, Q4Warp &W, double *acc, const uint8_t *smb, int sbo, int i,
+                                        int gl, int r, int &run) {
+  constexpr int G = Q4_G;
+  const int64_t *arp = SRC ? op.ao_rp : op.ad_rp;
+  const int32_t *acol = SRC ? op.ao_col : op.ad_col;
+  const double *aval = SRC ? op.ao_val : op.ad_val;
+  const int64_t *qrp = SRC ? op.pr_rp : op.pd_rp;
+  const double *qval = SRC ? op.pr_val : op.pd_val;
+  const bool po_here = SRC == 0 && op.po_rp != nullptr;
+  int t0 = 0, len = 0;
+  if (i >= 0) { t0 = (int)__ldg(arp + i); len = (int)__ldg(arp + i + 1) - t0; }
+  const int maxlen = __reduce_max_sync(FULL, len);
+#pragma unroll 1
+  for (int tb = 0; tb < maxlen; tb += G) {
+    const int t = tb + gl;
+    double a = 0.0;
+    int d0 = 0, o0 = 0, nd = 0, plen = 0;
+    if (t < len) {
+      const int k = __ldg(acol + t0 + t);
+      a = __ldg(aval + t0 + t);
+      d0 = (int)__ldg(qrp + k);
+      nd = plen = (int)__ldg(qrp + k + 1) - d0;
+      if (po_here) {
+        o0 = (int)__ldg(op.po_rp + k);
+        plen += (int)__ldg(op.po_rp + k + 1) - o0;
+      }
+    }
+    int incl = plen;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o, G);
+      if (gl >= o) incl += y;
+    }
+    W.a[gl][r] = a;
+    W.dp[gl][r] = make_int2(d0, (int)((uint32_t)(run + incl - plen) | ((uint32_t)nd << 16) | ((uint32_t)plen << 24)));
+    if (po_here) W.o0[gl][r] = o0;
+    run += __shfl_sync(FULL, incl, G - 1, G);
+    __syncwarp();
+    const int steps = min(G, maxlen - tb);
+    // P values and slots of all steps first (independent loads in flight
+    // together), then the folds in step order
+    double pv[G];
+    int sv[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      pv[j] = 0.0; sv[j] = 0;
+      if (j < steps) {
+        const int2 e = W.dp[j][r];
+        const int plj = (int)((uint32_t)e.y >> 24), ndj = (e.y >> 16) & 0xff;
+        if (gl < plj) {
+          pv[j] = gl < ndj ? __ldg(qval + e.x + gl) : __ldg(op.po_val + W.o0[j][r] + (gl - ndj));
+          sv[j] = smb[sbo + (e.y & 0xffff) + gl];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (j < steps) {
+        const int2 e = W.dp[j][r];
+        const int plj = (int)((uint32_t)e.y >> 24);
+        if (gl < plj) {
+          const double aj = W.a[j][r];
+          const int s = sv[j], sl = s & 0x7f;
+          const double prod = __dmul_rn(aj, pv[j]);
+          acc[sl] = (s & 0x80) ? prod : __dadd_rn(acc[sl], prod);
+          if (plj > G) {  // P rows longer than the group
+            const int ndj = (e.y >> 16) & 0xff, off = sbo + (e.y & 0xffff);
+            for (int u = gl + G; u < plj; u += G) {
+              const double p = u < ndj ? __ldg(qval + e.x + u) : __ldg(op.po_val + W.o0[j][r] + (u - ndj));
+              const int s2 = smb[off + u], sl2 = s2 & 0x7f;
+              const double pr2 = __dmul_rn(aj, p);
+              acc[sl2] = (s2 & 0x80) ? pr2 : __dadd_rn(acc[sl2], pr2);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_q4(Ops op, const int32_t *rows,
+                                                                      unsigned long long nrows, MapArgs mp,
+                                                                      OuterTargets tg, int do_send, int do_local,
+                                                                      int *status) {
+  // 32-bit offsets throughout (the plan checks every array fits): 64-bit
+  // live values would spill
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int G = Q4_G, NREG = Q4_CAP / Q4_G;
+  const int lane = lane_id(), gl = lane & (G - 1), r = lane / G;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  double *acc = (double *)smem + (warp * Q4_RPW + r) * Q4_ACC;
+  Q4Warp &W = ((Q4Warp *)((double *)smem + nwarps * Q4_RPW * Q4_ACC))[warp];
+  const uint8_t *smb = (const uint8_t *)W.sm;
+  const bool has_po = op.po_rp != nullptr;
+  const int total = (int)nrows;
+  for (int r0 = (blockIdx.x * nwarps + warp) * Q4_RPW; r0 < total; r0 += gridDim.x * nwarps * Q4_RPW) {
+    const int ridx = r0 + r;
+    int i = ridx < total ? (rows ? rows[ridx] : ridx) : -1;
+    const int i0 = __shfl_sync(FULL, i, 0);
+    const bool contig = __all_sync(FULL, i >= 0 && i == i0 + r);
+    bool wl = false, ws = false;
+    if (i >= 0) {
+      wl = do_local && __ldg(op.pd_rp + i + 1) > __ldg(op.pd_rp + i);
+      ws = do_send && has_po && __ldg(op.po_rp + i + 1) > __ldg(op.po_rp + i);
+    }
+    const int sb = i >= 0 ? (int)__ldg(mp.smap_rp + i) : 0;
+    // slot maps -> shared: one coalesced sweep for a consecutive batch, else
+    // row by row (the plan guarantees <= 128 map bytes per row)
+    int sbo;
+    __syncwarp();
+    if (contig) {
+      const int wb0 = __shfl_sync(FULL, sb, 0) >> 2;
+      const int we = ((int)__ldg(mp.smap_rp + i0 + Q4_RPW) + 3) >> 2;
+      const uint32_t *src = (const uint32_t *)mp.smap + wb0;
+      for (int q = lane; q < we - wb0; q += 32) W.sm[q] = __ldg(src + q);
+      sbo = sb - wb0 * 4;
+    } else {
+      if (i >= 0) {
+        const int wb = sb >> 2, we = ((int)__ldg(mp.smap_rp + i + 1) + 3) >> 2;
+        const uint32_t *src = (const uint32_t *)mp.smap + wb;
+        for (int q = gl; q < we - wb; q += G) W.sm[r * 33 + q] = __ldg(src + q);
+      }
+      sbo = r * 132 + (sb & 3);
+    }
+    if (!(wl || ws)) i = -1;
+    __syncwarp();
+    if (__all_sync(FULL, i < 0)) continue;
+    int run = 0;
+    q4_fold<0>(op, W, acc, smb, sbo, i, gl, r, run);
+    if (op.ao_rp != nullptr) q4_fold<1>(op, W, acc, smb, sbo, i, gl, r, run);
+    int64_t pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
+    int nap = 0;
+    if (i >= 0) {
+      pd0 = __ldg(op.pd_rp + i); pd1 = __ldg(op.pd_rp + i + 1);
+      if (has_po) { po0 = __ldg(op.po_rp + i); po1 = __ldg(op.po_rp + i + 1); }
+      nap = (int)__ldg(mp.nap + i);  // <= 32: first-touch flags valid
+    }
+    double accr[NREG];
+#pragma unroll
+    for (int q = 0; q < NREG; ++q) accr[q] = (gl + G * q < nap) ? acc[gl + G * q] : 0.0;
+    outer_scatter<G, NREG>(op, mp, tg, i, pd0, pd1, po0, po1, wl, ws, nap, accr, gl);
+  }
+}
+
 // Grid size of the grid-stride numeric kernels: PTAP_GRID_RESIDENT=1 caps the
 // grid at the resident CTA count (one contiguous band of rows in flight);
 // the default oversubscribes the grid (148 x 64 CTAs).
@@ -380,10 +563,17 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
   if (nrows == 0) return cudaSuccess;
   const int warps = 8;
   cudaError_t e;
-  if (bin == 0) {
+  if (bin == 3) {  // bin 0 through the 32-bit q4 kernel (eligibility checked by the plan)
+    const size_t sm = q4_smem(warps);
+    if ((e = opt_in(k_outer_numeric_q4, sm)) != cudaSuccess) return e;
+    const unsigned long long rpc = (unsigned long long)warps * Q4_RPW;
+    unsigned long long grid = (nrows + rpc - 1) / rpc;
+    grid = std::min(grid, grid_cap(k_outer_numeric_q4, warps * 32, sm));
+    k_outer_numeric_q4<<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local, status);
+  } else if (bin == 0) {
     constexpr int G = 4, CAP = 32;
     const int gpc = warps * (32 / G);
-    size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
+    size_t sm = (size_t)gpc * group_bytes(G, CAP);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
     grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
@@ -392,7 +582,7 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
   } else {
     constexpr int G = 32, CAP = 256;
     const int gpc = warps;
-    size_t sm = (size_t)gpc * ((((size_t)(CAP + 1) * 8 + 15) & ~(size_t)15) + G * 16 + G * 4 + 15 & ~(size_t)15);
+    size_t sm = (size_t)gpc * group_bytes(G, CAP);
     if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
     unsigned long long grid = (nrows + gpc - 1) / gpc;
     grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
