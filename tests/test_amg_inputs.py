@@ -1,0 +1,95 @@
+"""Configs 4 and 5 (smoothed-aggregation P) at reduced size: generator
+invariants on the CPU, the oracle on them, and CUDA parity (``-m gpu``)."""
+
+import numpy as np
+import pytest
+
+from paper_1905_08423_b200 import problems_amg as amg
+from tests.conftest import row_scaled_err, run_ptap
+
+TOL = 1e-12
+
+
+def _dense(m):
+    d = np.zeros((m.nrows, m.ncols))
+    for i in range(m.nrows):
+        d[i, m.row_cols(i)] = m.row_values(i)
+    return d
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    return amg.block_transport(6)
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    return amg.knn_laplacian(3000)
+
+
+@pytest.fixture(scope="module")
+def cfg4_wide():
+    """12^3 nodes: C rows up to ~270 entries, past the byte-map limit, so the
+    hash numeric path runs."""
+    return amg.block_transport(12)
+
+
+@pytest.fixture(scope="module")
+def cfg5_large():
+    return amg.knn_laplacian(20000)
+
+
+def test_cfg4_generator_invariants(cfg4):
+    A, P = cfg4
+    assert A.nrows == 6 ** 3 * 10 and P.ncols == 2 ** 3 * 10
+    d = _dense(A)
+    assert np.array_equal(d, d.T), "A symmetric"
+    off = np.abs(d).sum(axis=1) - np.abs(np.diag(d))
+    assert np.all(np.diag(d) > off), "strictly diagonally dominant"
+    assert np.all(np.diff(P.row_offsets) > 0)
+    A2, P2 = amg.block_transport(6)
+    assert np.array_equal(A.values.view(np.uint64), A2.values.view(np.uint64))
+    assert np.array_equal(P.values.view(np.uint64), P2.values.view(np.uint64))
+
+
+def test_cfg5_generator_invariants(cfg5):
+    A, P = cfg5
+    d = _dense(A)
+    assert np.allclose(d, d.T, rtol=0, atol=0), "A symmetric"
+    assert np.all(np.abs(np.diag(d) - (-(d - np.diag(np.diag(d))).sum(axis=1)) - 1e-3) < 1e-9), "Laplacian + 1e-3"
+    deg = np.diff(A.row_offsets) - 1
+    assert deg.min() >= 26, "every point keeps its 26 nearest neighbours"
+    assert 20 < A.nrows / P.ncols < 120, "aggregation coarsening"
+    assert np.all(np.diff(P.row_offsets) > 0)
+
+
+@pytest.mark.parametrize("which", ["cfg4", "cfg5"])
+def test_oracle_on_amg_inputs_matches_dense(which, request):
+    """The oracle (pinned on the reference's goldens) on these inputs agrees
+    with a dense P^T A P; this is the check the GPU tests then lean on."""
+    from oracle.oracle import oracle_ptap
+    A, P = request.getfixturevalue(which)
+    w = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values, P.row_offsets,
+                    P.col_indices, P.values, nranks=2, algorithm="allatonce")
+    dense = _dense(P).T @ _dense(A) @ _dense(P)
+    got = np.zeros_like(dense)
+    for i in range(P.ncols):
+        got[i, w.col[w.row_ptr[i]:w.row_ptr[i + 1]]] = w.val[w.row_ptr[i]:w.row_ptr[i + 1]]
+    assert np.max(np.abs(got - dense)) <= 1e-12 * np.max(np.abs(dense))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["cfg4", "cfg5", "cfg4_wide", "cfg5_large"])
+@pytest.mark.parametrize("nr", [1, 2])
+@pytest.mark.parametrize("alg", ["two-step", "allatonce", "merged"])
+def test_gpu_parity_amg_inputs(which, nr, alg, request):
+    from oracle.oracle import oracle_ptap
+    A, P = request.getfixturevalue(which)
+    want = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values, P.row_offsets,
+                       P.col_indices, P.values, nranks=nr, algorithm=alg)
+    c, _ = run_ptap(A, P, nr, alg)
+    assert np.array_equal(c.row_offsets, want.row_ptr)
+    assert np.array_equal(c.col_indices, want.col)
+    if alg == "two-step":
+        assert np.array_equal(c.values.view(np.uint64), want.val.view(np.uint64))
+    assert row_scaled_err(want.row_ptr, c.values, want.val) <= TOL
