@@ -323,17 +323,13 @@ def spawn_ranks(nranks: int, program, *, backend: str = "gloo", timeout: float =
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    torch = _torch()
-    if torch.cuda.is_available() and torch.cuda.is_initialized():
-        # CUDA cannot be re-initialised in a forked child: spawn, shipping the
-        # program (usually a closure) by value
-        import cloudpickle
+    # fresh interpreters (spawn): a forked child inherits the parent's CUDA
+    # context and OpenMP thread-pool state, either of which can hang it; the
+    # program (usually a closure) is shipped by value
+    import cloudpickle
 
-        mpctx = mp.get_context("spawn")
-        payload = cloudpickle.dumps(program)
-    else:
-        mpctx = mp.get_context("fork")
-        payload = program
+    mpctx = mp.get_context("spawn")
+    payload = cloudpickle.dumps(program)
     q = mpctx.Queue()
     procs = [mpctx.Process(target=_rank_main, args=(r, nranks, port, payload, q, backend)) for r in range(nranks)]
     for p in procs:
