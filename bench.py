@@ -300,13 +300,23 @@ def our_arm(args):
         return plan, max_over_ranks(time.perf_counter() - t, ctx, torch)
 
     # --- headline: all-at-once ------------------------------------------------
-    plan, sym_cold = symbolic("allatonce")   # first call: includes one-time module/pool setup
-    del plan
     import gc
 
-    gc.collect()
-    torch.cuda.synchronize()
-    plan, sym_s = symbolic("allatonce")
+    def warm_symbolic(alg):
+        """cold call (one-time module and memory-pool setup), then two warm
+        calls; the warm figure is the faster of the two (the host-side driver
+        calls occasionally stall for ~0.1 s on these boxes)"""
+        pl, cold = symbolic(alg)
+        warm = []
+        for _ in range(2):
+            del pl
+            gc.collect()
+            torch.cuda.synchronize()
+            pl, t = symbolic(alg)
+            warm.append(t)
+        return pl, cold, min(warm), warm
+
+    plan, sym_cold, sym_s, sym_all = warm_symbolic("allatonce")
     cnt = plan.device_counters()
     mac = sum_over_ranks(cnt["mac_ap"] + cnt["mac_outer"], ctx, torch)
     flops = 2.0 * mac
@@ -324,21 +334,10 @@ def our_arm(args):
     kms = statistics.mean(kern_ms) if kern_ms else ms
     achieved = my_bytes / (kms * 1e-3) / 1e9
     out["allatonce"] = {"numeric_ms": ms, "symbolic_ms": sym_s * 1e3, "symbolic_cold_ms": sym_cold * 1e3,
+                        "symbolic_warm_runs_ms": [t * 1e3 for t in sym_all],
+                        "ptap_wall_ms": sym_s * 1e3 + ms,
                         "aux_peak_bytes": mem["device_high_water"] - mem["current"]["output_matrix"],
                         "memory": mem}
-
-    # --- variants -------------------------------------------------------------
-    if not args.no_variants:
-        for alg in ("merged", "two-step"):
-            vplan, vsym = symbolic(alg)
-            vms, _, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
-            vmem = vplan.memory()
-            out[alg] = {"numeric_ms": max_over_ranks(vms, ctx, torch), "symbolic_ms": vsym * 1e3,
-                        "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
-                        "memory": vmem}
-            del vplan
-            gc.collect()
-            torch.cuda.synchronize()
 
     # --- config 3 level 2: A2 = C1 kept on the device (hierarchy driver), P2 trilinear
     level2 = None
@@ -373,6 +372,26 @@ def our_arm(args):
     if not args.no_e2e:
         e2e = e2e_leg(pk, a, p, plan, ctx, flops, max(3, min(args.steps, 5)), torch)
 
+    # --- variants (headline plan released first so every variant's warm
+    # symbolic phase sees the same memory pool state) -----------------------------
+    del plan, c_rp, c_col, c_val
+    gc.collect()
+    torch.cuda.synchronize()
+    if not args.no_variants:
+        for alg in ("merged", "two-step"):
+            vplan, vcold, vsym, vall = warm_symbolic(alg)
+            vms, _, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
+            vmem = vplan.memory()
+            vms = max_over_ranks(vms, ctx, torch)
+            out[alg] = {"numeric_ms": vms, "symbolic_ms": vsym * 1e3, "symbolic_cold_ms": vcold * 1e3,
+                        "symbolic_warm_runs_ms": [t * 1e3 for t in vall],
+                        "ptap_wall_ms": vsym * 1e3 + vms,
+                        "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
+                        "memory": vmem}
+            del vplan
+            gc.collect()
+            torch.cuda.synchronize()
+
     # --- CPU baseline (rank 0, N = 1) -----------------------------------------
     cpu = None
     if ctx.rank == 0 and ctx.nranks == 1 and not args.no_cpu_baseline:
@@ -395,7 +414,7 @@ def our_arm(args):
                        "gen_s": gen_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_outer_numeric (ptap_numeric_local)", "kernel_ms": kms,
+                         "kernel": "k_outer_numeric_q4 (ptap_numeric_local)", "kernel_ms": kms,
                          "alg_bytes_per_launch": my_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -43,7 +43,15 @@ struct Tracer {
     if (!on) return;
     cudaStreamSynchronize(st);
     auto t1 = std::chrono::steady_clock::now();
-    fprintf(stderr, "[ptap] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    unsigned long long reserved = 0, used = 0;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    fprintf(stderr, "[ptap] %-28s %9.3f ms   pool reserved %.2f GB used %.2f GB\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t0).count(), reserved / 1e9, used / 1e9);
     t0 = t1;
   }
 };
