@@ -341,15 +341,19 @@ ptap_status arena_grow(ptap_plan *p, Arena &ar, cudaStream_t st) {
 ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, int64_t **rp_out, int32_t **col_out,
                          int64_t *nnz_out, int64_t **cnt_keep, cudaStream_t st) {
   int64_t *cnt = nullptr, *rp = nullptr, *scratch = nullptr;
+  Tracer tr;
+  tr.on = tr.on && getenv("PTAP_TRACE")[0] == '2';
   CKS(palloc(p, &cnt, nrows_dense, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nrows_dense > 0 ? nrows_dense : 1), st));
   CK(launch_arena_rowcount(ar, p->m, cnt, st));
+  tr.mark(st, "  drain: rowcount");
   CKS(palloc(p, &rp, nrows_dense + 1, cat, st));
   CKS(palloc(p, &scratch, scan_scratch_elems(nrows_dense), CAT_TRANSIENT, st));
   CK(scan_exclusive(cnt, rp, nrows_dense, scratch, st));
   int64_t nnz = 0;
   CK(cudaMemcpyAsync(&nnz, rp + nrows_dense, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  tr.mark(st, "  drain: scan");
   int32_t *col = nullptr;
   CKS(palloc(p, &col, nnz, cat, st));
   int64_t *cursor = scratch;  // reuse: needs nrows_dense entries
@@ -358,6 +362,7 @@ ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, i
   CK(cudaMemsetAsync(cursor, 0, sizeof(int64_t) * (nrows_dense > 0 ? nrows_dense : 1), st));
   CK(launch_arena_scatter(ar, p->m, rp, cursor, col, st));
   pfree(p, cursor, st);
+  tr.mark(st, "  drain: scatter");
   int32_t *wide = nullptr;
   CKS(palloc(p, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(p->d_u64 + 6, 0, sizeof(unsigned long long), st));
@@ -365,7 +370,9 @@ ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, i
   unsigned long long nwide = 0;
   CK(cudaMemcpyAsync(&nwide, p->d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  tr.mark(st, "  drain: sort rows");
   CK(launch_sort_rows_block((int64_t)nwide, wide, rp, col, nullptr, p->d_status, st));
+  tr.mark(st, "  drain: sort wide");
   pfree(p, wide, st);
   p->cnt.kernel_launches += 6;
   if (cnt_keep) *cnt_keep = cnt; else pfree(p, cnt, st);
@@ -448,15 +455,30 @@ ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStre
   CK(launch_row_work(op, apub, p->d_u64 + 7, st));
   unsigned long long mac_ap = 0;
   CK(cudaMemcpyAsync(&mac_ap, p->d_u64 + 7, sizeof(mac_ap), cudaMemcpyDeviceToHost, st));
-  BinSet tmp;
-  CKS(build_bins(p, tmp, op.nloc, apub, op.pd_rp, op.po_rp, 0, false, CAT_TRANSIENT, st));
   p->cnt.mac_ap = (int64_t)mac_ap;
   CKS(palloc(p, &ap_nnz, op.nloc, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(ap_nnz, 0, sizeof(int64_t) * (op.nloc > 0 ? op.nloc : 1), st));
+  // optimistic small-table count first; rows that do not fit are recounted
+  // through the work bins
+  const int64_t *est = apub;
+  int64_t *est2 = nullptr;
+  int mode = 0;
+  if (!getenv("PTAP_NO_FASTCOUNT")) {
+    CK(launch_ap_count_small(op, op.nloc, apub, ap_nnz, st));
+    CKS(palloc(p, &est2, op.nloc, CAT_TRANSIENT, st));
+    CK(cudaMemsetAsync(p->d_u64 + 16, 0, sizeof(unsigned long long), st));
+    CK(launch_retry_est(op.nloc, ap_nnz, apub, est2, p->d_u64 + 16, st));
+    p->cnt.kernel_launches += 2;
+    est = est2;
+    mode = 4;
+  }
+  BinSet tmp;
+  CKS(build_bins(p, tmp, op.nloc, est, op.pd_rp, op.po_rp, mode, false, CAT_TRANSIENT, st));
   CKS(for_bins(p, tmp, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
     return launch_ap_count(s, op, rows, n, ap_nnz, p->d_status, st);
   }));
   free_bins(p, tmp, st);
+  pfree(p, est2, st);
   if (apub_out) *apub_out = apub; else pfree(p, apub, st);
   // bounds of the outer products
   CK(cudaMemsetAsync(p->d_u64 + 8, 0, 3 * sizeof(unsigned long long), st));
@@ -1001,7 +1023,7 @@ ptap_status ptap_spgemm_ap_symbolic(const ptap_operands *ops, int64_t *nnz_out, 
   ptap_plan tmp;
   tmp.nloc = ops->n_local; tmp.m = ops->m_global; tmp.c_lo = ops->c_lo; tmp.c_hi = ops->c_hi;
   if (cudaMalloc(&tmp.d_status, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&tmp.d_u64, 16 * sizeof(unsigned long long)) != cudaSuccess)
+      cudaMalloc(&tmp.d_u64, 24 * sizeof(unsigned long long)) != cudaSuccess)
     return fail(PTAP_ERR_CUDA, "alloc");
   cudaMemset(tmp.d_status, 0, sizeof(int));
   Ops op = make_ops(ops);
@@ -1059,7 +1081,7 @@ ptap_status ptap_spgemm_ap_numeric(const ptap_operands *ops, const int64_t *row_
   ptap_plan tmp;
   tmp.nloc = ops->n_local; tmp.m = ops->m_global;
   if (cudaMalloc(&tmp.d_status, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&tmp.d_u64, 16 * sizeof(unsigned long long)) != cudaSuccess)
+      cudaMalloc(&tmp.d_u64, 24 * sizeof(unsigned long long)) != cudaSuccess)
     return fail(PTAP_ERR_CUDA, "alloc");
   cudaMemset(tmp.d_status, 0, sizeof(int));
   Ops op = make_ops(ops);

@@ -13,6 +13,7 @@
 //   k_transpose_*         stable transpose of P blocks with permutation      sparse.py:165-178
 //   k_ptc_symbolic        two-step P^T C~ structure                          _kernels.py:558-580
 //   k_ptc_numeric<G>      two-step P^T C~ values (staging or C)              _kernels.py:583-677
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -56,7 +57,8 @@ __global__ void k_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd_
   if (i < nrows) {
     bool pd = pd_rp && pd_rp[i + 1] > pd_rp[i];
     bool po = po_rp && po_rp[i + 1] > po_rp[i];
-    bool want = mode == 0 || (mode == 1 && po) || (mode == 2 && pd) || (mode == 3 && (po || pd));
+    bool want = mode == 0 || (mode == 1 && po) || (mode == 2 && pd) || (mode == 3 && (po || pd)) ||
+                (mode == 4 && est[i] >= 0);
     if (want) {
       int64_t n = est[i];
       b = NBINS - 1;
@@ -166,6 +168,62 @@ __global__ void __launch_bounds__(256) k_ap_count(Ops op, const int32_t *rows, u
     if (i >= 0 && (lane_id() & (GROUP - 1)) == 0) ap_nnz[i] = nnew;
     __syncwarp();
   }
+}
+
+// Optimistic AP row count: 4 lanes and one 64-slot shared table per row, 8
+// rows per warp, over every row of the block.  A row whose distinct columns
+// do not fit (or whose pair count exceeds 256) gets -1 and is recounted by
+// the binned k_ap_count; on stencil-like inputs no row is.
+constexpr int APC_G = 4, APC_LOG2T = 6;
+__global__ void __launch_bounds__(256) k_ap_count_small(Ops op, int64_t nrows, const int64_t *apub,
+                                                        int64_t *ap_nnz) {
+  constexpr int T = 1 << APC_LOG2T, GPC = 256 / APC_G;
+  __shared__ int32_t keys_all[GPC][T];
+  __shared__ int fail_all[GPC];
+  const int gid = threadIdx.x / APC_G;
+  int32_t *keys = keys_all[gid];
+  int *fail = fail_all + gid;
+  PStage ps{nullptr, nullptr};
+  for (int64_t r0 = (int64_t)blockIdx.x * GPC; r0 < nrows; r0 += (int64_t)gridDim.x * GPC) {
+    int64_t i = r0 + gid;
+    if (i >= nrows || __ldg(apub + i) > 256) i = -1;
+    table_clear<APC_G>(keys, T);
+    if ((lane_id() & (APC_G - 1)) == 0) *fail = 0;
+    __syncwarp();
+    int nnew = ap_row_accumulate<APC_G, false>(op, i, keys, nullptr, APC_LOG2T, ps, fail);
+    nnew = group_sum<APC_G>(nnew);
+    __syncwarp();
+    if ((lane_id() & (APC_G - 1)) == 0) {
+      const int64_t r = r0 + gid;
+      if (r < nrows) ap_nnz[r] = (i < 0 || *fail) ? -1 : nnew;
+    }
+    __syncwarp();
+  }
+}
+
+// est2[i] = apub[i] for rows the optimistic count left at -1, else -1
+__global__ void k_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *apub, int64_t *est2,
+                            unsigned long long *nretry) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool r = i < n && ap_nnz[i] < 0;
+  if (i < n) est2[i] = r ? apub[i] : -1;
+  unsigned b = __ballot_sync(FULL, r);
+  if (lane_id() == 0 && b) atomicAdd(nretry, (unsigned long long)__popc(b));
+}
+
+cudaError_t launch_ap_count_small(const Ops &op, int64_t nrows, const int64_t *apub, int64_t *ap_nnz,
+                                  cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  int64_t blocks = (nrows + 63) / 64;
+  int grid = (int)std::min<int64_t>(blocks, 148 * 32);
+  k_ap_count_small<<<grid, 256, 0, st>>>(op, nrows, apub, ap_nnz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *apub, int64_t *est2,
+                             unsigned long long *nretry, cudaStream_t st) {
+  if (n > 0) k_retry_est<<<(int)((n + 255) / 256), 256, 0, st>>>(n, ap_nnz, apub, est2, nretry);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

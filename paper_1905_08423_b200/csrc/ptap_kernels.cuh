@@ -72,6 +72,10 @@ cudaError_t launch_bin_rows(int64_t nrows, const int64_t *est, const int64_t *pd
                             const BinLists &bl, unsigned long long *selected, cudaStream_t st);
 cudaError_t launch_max_est(const int32_t *rows, unsigned long long nrows, const int64_t *est, unsigned long long *mx,
                            cudaStream_t st);
+cudaError_t launch_ap_count_small(const Ops &op, int64_t nrows, const int64_t *apub, int64_t *ap_nnz,
+                                  cudaStream_t st);
+cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *apub, int64_t *est2,
+                             unsigned long long *nretry, cudaStream_t st);
 cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                             int64_t *ap_nnz, int *status, cudaStream_t stream);
 cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
