@@ -317,11 +317,23 @@ ptap_status for_bins(ptap_plan *p, BinSet &bs, F launch) {
 }
 
 // ---- arenas ------------------------------------------------------------------
-ptap_status arena_alloc(ptap_plan *p, Arena &ar, unsigned long long min_keys, cudaStream_t st) {
+// bucket_rows > 0: the keys' rows are [0, bucket_rows) (a local C arena) and
+// each row gets its own run of slots when the capacity allows >= 8 per row
+ptap_status arena_alloc(ptap_plan *p, Arena &ar, unsigned long long min_keys, cudaStream_t st,
+                        unsigned long long bucket_rows = 0) {
   unsigned long long cap = 1024;
   while (cap * 3 < min_keys * 4) cap <<= 1;  // <= 75% load at the estimate
   CKS(palloc(p, &ar.keys, (int64_t)cap, CAT_TRANSIENT, st));
   ar.mask = cap - 1;
+  ar.m = (unsigned long long)p->m;
+  ar.log2b = 0;
+  if (bucket_rows > 0 && !getenv("PTAP_HASHED_ARENA")) {
+    unsigned long long r = 1;
+    while (r < bucket_rows) r <<= 1;
+    int lb = 0;
+    while ((r << (lb + 1)) <= cap) ++lb;
+    ar.log2b = lb >= 3 ? lb : 0;
+  }
   CK(launch_arena_fill_empty(ar, st));
   p->cnt.kernel_launches++;
   return PTAP_OK;
@@ -329,7 +341,7 @@ ptap_status arena_alloc(ptap_plan *p, Arena &ar, unsigned long long min_keys, cu
 
 ptap_status arena_grow(ptap_plan *p, Arena &ar, cudaStream_t st) {
   Arena big{nullptr, 0};
-  CKS(arena_alloc(p, big, 2 * (ar.mask + 1), st));
+  CKS(arena_alloc(p, big, 2 * (ar.mask + 1), st, ar.log2b > 0 ? (ar.mask + 1) >> ar.log2b : 0));
   CK(launch_arena_rehash(ar, big, p->d_status, st));
   p->cnt.kernel_launches++;
   pfree(p, ar.keys, st);
@@ -762,7 +774,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     }
     Arena send{nullptr, 0};
     CKS(arena_alloc(p, send, p->bound_send + 16, st));
-    if (merged) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, 0), st));
+    if (merged) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, 0), st, (unsigned long long)p->ncl));
     BinSet &bs = merged ? p->bins_all : p->bins_send;
     auto pass = [&]() -> ptap_status {
       return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
@@ -816,7 +828,8 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   Ops op = make_ops(ops);
   int64_t rnnz = recv ? recv->nnz : 0;
   Tracer tr;
-  if (p->alg != PTAP_MERGED) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st));
+  if (p->alg != PTAP_MERGED)
+    CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st, (unsigned long long)p->ncl));
   tr.mark(st, "local arena alloc");
   Arena &la = p->local_arena;
   if (p->alg == PTAP_ALLATONCE) {

@@ -229,9 +229,23 @@ cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *ap
 // ---------------------------------------------------------------------------
 // arenas
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void arena_insert(unsigned long long *ar, unsigned long long mask, unsigned long long key,
+// Insert key = row * m + col.  Row-bucketed arenas (log2b > 0, the local
+// C arenas) place row r's keys in its own run of 2^log2b slots (the column
+// hashed inside it): the ~13 inserts per C entry then hit the same few lines,
+// which neighbouring fine rows (processed together) keep hot in L2, instead
+// of one random DRAM line per insert.  Overflow probes linearly, as in the
+// hashed mode.
+__device__ __forceinline__ void arena_insert(const Arena &a, unsigned long long row, unsigned long long col,
                                              int *status) {
-  unsigned long long h = hash64(key) & mask;
+  const unsigned long long key = row * a.m + col;
+  unsigned long long h;
+  if (a.log2b > 0) {
+    const unsigned long long bm = (1ull << a.log2b) - 1ull;
+    h = ((row << a.log2b) | ((unsigned long long)hash32((uint32_t)col, a.log2b) & bm)) & a.mask;
+  } else {
+    h = hash64(key) & a.mask;
+  }
+  unsigned long long *ar = a.keys;
   for (int probe = 0; probe < 8192; ++probe) {
     unsigned long long k = ar[h];
     if (k == key) return;
@@ -239,7 +253,7 @@ __device__ __forceinline__ void arena_insert(unsigned long long *ar, unsigned lo
       unsigned long long old = atomicCAS(ar + h, EMPTY64, key);
       if (old == EMPTY64 || old == key) return;
     }
-    h = (h + 1) & mask;
+    h = (h + 1) & a.mask;
   }
   atomicOr(status, ST_ARENA_FULL);
 }
@@ -257,7 +271,6 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
   const int gpc = (blockDim.x >> 5) * gpw;
   const int T = 1 << log2t;
   const int gl = lane_id() & (GROUP - 1);
-  const unsigned long long m = (unsigned long long)op.m;
   const bool maps = mo.smap != nullptr;
   for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
        r0 += (unsigned long long)gridDim.x * gpc) {
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
         for (int f = gl; f < tot; f += GROUP) {
           int jj = f / n, e = f - jj * n;
           unsigned long long J = (unsigned long long)op.pd_col[pd0 + jj];
-          arena_insert(local.keys, local.mask, J * m + (unsigned long long)tb.lk[e], status);
+          arena_insert(local, J, (unsigned long long)tb.lk[e], status);
         }
       }
       if (ws) {
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
         for (int f = gl; f < tot; f += GROUP) {
           int jj = f / n, e = f - jj * n;
           unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[po0 + jj]];
-          arena_insert(send.keys, send.mask, J * m + (unsigned long long)tb.lk[e], status);
+          arena_insert(send, J, (unsigned long long)tb.lk[e], status);
         }
       }
     }
@@ -385,9 +398,8 @@ __global__ void k_arena_insert_batch(Arena ar, int64_t nrows, const int32_t *row
   if (w >= nrows) return;
   int32_t J = rows[w];
   if (J < c_lo || J >= c_hi) { if (lane_id() == 0) atomicOr(status, ST_DRIFT); return; }
-  unsigned long long base = (unsigned long long)(J - c_lo) * (unsigned long long)m;
-  for (int64_t e = rp[w] + lane_id(); e < rp[w + 1]; e += 32)
-    arena_insert(ar.keys, ar.mask, base + (unsigned long long)col[e], status);
+  const unsigned long long r = (unsigned long long)(J - c_lo);
+  for (int64_t e = rp[w] + lane_id(); e < rp[w + 1]; e += 32) arena_insert(ar, r, (unsigned long long)col[e], status);
 }
 
 __global__ void k_arena_rowcount(Arena ar, unsigned long long m, int64_t *cnt) {
@@ -684,7 +696,7 @@ __global__ void k_ptc_symbolic(int64_t nrows, const int64_t *t_rp, const int32_t
   for (int64_t t = t_rp[w]; t < t_rp[w + 1]; ++t) {
     int32_t i = t_row[t];
     for (int64_t e = ct_rp[i] + lane_id(); e < ct_rp[i + 1]; e += 32)
-      arena_insert(ar.keys, ar.mask, tgt * m + (unsigned long long)ct_col[e], status);
+      arena_insert(ar, tgt, (unsigned long long)ct_col[e], status);
   }
 }
 
@@ -877,7 +889,7 @@ __global__ void k_arena_rehash(Arena from, Arena to, int *status) {
   unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (s > from.mask) return;
   unsigned long long k = from.keys[s];
-  if (k != EMPTY64) arena_insert(to.keys, to.mask, k, status);
+  if (k != EMPTY64) arena_insert(to, k / to.m, k % to.m, status);
 }
 
 // exact table sizes for the two-step P^T C~ rows: the length of the target

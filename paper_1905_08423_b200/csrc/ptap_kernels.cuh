@@ -23,6 +23,8 @@ struct BinLists {
 struct Arena {
   unsigned long long *keys;
   unsigned long long mask;  // capacity - 1 (power of two)
+  int log2b = 0;            // > 0: row-bucketed placement (2^log2b slots per row), 0: hashed
+  unsigned long long m = 0; // key = row * m + col
 };
 
 struct OuterTargets {
