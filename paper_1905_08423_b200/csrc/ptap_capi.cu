@@ -538,6 +538,8 @@ ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
 // slot maps are written by that pass itself, so allocate them here.
 ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
   p->want_maps = false;
+  Tracer tr;
+  tr.on = tr.on && getenv("PTAP_TRACE")[0] == '2';
   if (getenv("PTAP_NO_MAPS")) return PTAP_OK;
   unsigned long long *mx = p->d_u64 + 12;
   CK(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), st));
@@ -548,6 +550,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   p->cnt.kernel_launches += 3;
+  tr.mark(st, "  maps: maxima");
   if (h[0] > 255 || h[1] > 65535 || h[2] > 255) return PTAP_OK;  // hash path for this plan
   {
     // bin 0 through k_outer_numeric_q4: <= 128 map bytes per row and every
@@ -562,6 +565,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
   int64_t *unused = nullptr;
   CKS(palloc(p, &unused, p->nloc, CAT_TRANSIENT, st));
+  tr.mark(st, "  maps: alloc 1");
   CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, slen, unused, st));
   CKS(palloc(p, &p->maps.smap_rp, p->nloc + 1, CAT_PLAN, st));
   CK(scan_exclusive(slen, p->maps.smap_rp, p->nloc, scratch, st));
@@ -571,6 +575,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   CK(cudaMemcpyAsync(&tot[0], p->maps.smap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&tot[1], p->pat_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  tr.mark(st, "  maps: lengths + scans");
   pfree(p, slen, st);
   pfree(p, unused, st);
   pfree(p, scratch, st);
@@ -578,6 +583,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   CKS(palloc(p, &p->maps.smap, tot[0] + 16, CAT_PLAN, st));  // padded: staged word-wise
   CKS(palloc(p, &p->maps.nap, p->nloc, CAT_PLAN, st));
   CKS(palloc(p, &p->pat, tot[1], CAT_TRANSIENT, st));
+  tr.mark(st, "  maps: alloc 2");
   p->mo = MapOut{p->maps.smap_rp, p->maps.smap, p->maps.nap, p->pat_rp, p->pat};
   p->want_maps = true;
   return PTAP_OK;

@@ -291,52 +291,62 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
       int P2 = 1;
       while (P2 < n) P2 <<= 1;
       int maxP2 = __reduce_max_sync(FULL, i >= 0 ? P2 : 1);
-      for (int x = gl; x < maxP2; x += GROUP) tb.sb[x] = (i >= 0 && x < n) ? tb.lk[x] : INT32_MAX;
-      __syncwarp();
-      for (int k = 2; k <= maxP2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int x = gl; x < maxP2; x += GROUP) {
-            int y = x ^ j;
-            if (y > x) {
-              bool up = (x & k) == 0;
-              int32_t kx = tb.sb[x], ky = tb.sb[y];
-              if ((kx > ky) == up) { tb.sb[x] = ky; tb.sb[y] = kx; }
-            }
+      if (maxP2 <= 64) {
+        // short rows: rank of every key = number of smaller keys (no sort)
+        if (i >= 0) {
+          int32_t *pat = mo.pat + mo.pat_rp[i];
+          for (int x = gl; x < n; x += GROUP) {
+            const int32_t g = tb.lk[x];
+            int rk = 0;
+            for (int y = 0; y < n; ++y) rk += tb.lk[y] < g;
+            pat[rk] = g;
+            tb.slot_of[table_find(tb.keys, log2t, g)] = rk;
           }
-          __syncwarp();
+          if (gl == 0) mo.nap[i] = (uint8_t)n;
         }
-      if (i >= 0) {
-        int32_t *pat = mo.pat + mo.pat_rp[i];
-        for (int x = gl; x < n; x += GROUP) {
-          int32_t g = tb.sb[x];
-          pat[x] = g;
-          tb.slot_of[table_find(tb.keys, log2t, g)] = x;
+        __syncwarp();
+      } else {
+        for (int x = gl; x < maxP2; x += GROUP) tb.sb[x] = (i >= 0 && x < n) ? tb.lk[x] : INT32_MAX;
+        __syncwarp();
+        for (int k = 2; k <= maxP2; k <<= 1)
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int x = gl; x < maxP2; x += GROUP) {
+              int y = x ^ j;
+              if (y > x) {
+                bool up = (x & k) == 0;
+                int32_t kx = tb.sb[x], ky = tb.sb[y];
+                if ((kx > ky) == up) { tb.sb[x] = ky; tb.sb[y] = kx; }
+              }
+            }
+            __syncwarp();
+          }
+        if (i >= 0) {
+          int32_t *pat = mo.pat + mo.pat_rp[i];
+          for (int x = gl; x < n; x += GROUP) {
+            int32_t g = tb.sb[x];
+            pat[x] = g;
+            tb.slot_of[table_find(tb.keys, log2t, g)] = x;
+          }
+          if (gl == 0) mo.nap[i] = (uint8_t)n;
         }
-        if (gl == 0) mo.nap[i] = (uint8_t)n;
+        __syncwarp();
       }
-      __syncwarp();
       for (int x = gl; x < maxP2; x += GROUP) tb.sb[x] = 0;  // seen[slot]
       __syncwarp();
       ap_row_write_smap<GROUP>(op, i, tb.keys, log2t, tb.slot_of, tb.sb, tb.ps,
                                mo.smap + (i >= 0 ? mo.smap_rp[i] : 0), n <= 127);
     }
     if (i >= 0 && n > 0) {
-      if (wl) {
-        int tot = (int)(pd1 - pd0) * n;
-        for (int f = gl; f < tot; f += GROUP) {
-          int jj = f / n, e = f - jj * n;
-          unsigned long long J = (unsigned long long)op.pd_col[pd0 + jj];
-          arena_insert(local, J, (unsigned long long)tb.lk[e], status);
+      if (wl)
+        for (int64_t jj = pd0; jj < pd1; ++jj) {
+          const unsigned long long J = (unsigned long long)__ldg(op.pd_col + jj);
+          for (int e = gl; e < n; e += GROUP) arena_insert(local, J, (unsigned long long)tb.lk[e], status);
         }
-      }
-      if (ws) {
-        int tot = (int)(po1 - po0) * n;
-        for (int f = gl; f < tot; f += GROUP) {
-          int jj = f / n, e = f - jj * n;
-          unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[po0 + jj]];
-          arena_insert(send, J, (unsigned long long)tb.lk[e], status);
+      if (ws)
+        for (int64_t jj = po0; jj < po1; ++jj) {
+          const unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[jj]];
+          for (int e = gl; e < n; e += GROUP) arena_insert(send, J, (unsigned long long)tb.lk[e], status);
         }
-      }
     }
     __syncwarp();
   }
