@@ -47,3 +47,38 @@ print("\ntop by L1 wavefronts (shared) / tags (global)")
 for r in sorted(data, key=lambda r: -(f(r, "L1 Wavefronts Shared") + f(r, "L1 Tag Requests Global")))[:15]:
     print(f"  {r[ix['Source']][:58]:58} inst/row={f(r,'Instructions Executed')/nrows:5.2f} shwf={f(r,'L1 Wavefronts Shared')/nrows:6.2f}"
           f" ideal={f(r,'L1 Wavefronts Shared Ideal')/nrows:5.2f} gtag={f(r,'L1 Tag Requests Global')/nrows:5.2f} l2s={f(r,'L2 Theoretical Sectors Global')/nrows:5.2f}")
+
+
+def write_summary(rep_path, kernel_desc, out_json, out_txt, nrows_):
+    """profiles/ncu_numeric_summary.json (read by bench.py for roofline.traffic)
+    and a text summary of the same capture."""
+    import json as _json
+    raw_ = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"],
+                                                      capture_output=True, text=True).stdout)))
+    R_ = dict(zip(raw_[0], raw_[2]))
+
+    def g(k):
+        try:
+            return float(R_[k].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+    rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
+    unit_scale = 1e9  # ncu reports dram bytes in GB in this layout
+    d = {"kernel": kernel_desc,
+         "capture": f"ncu --set full --clock-control none, 1 launch ({os.path.basename(out_txt)})",
+         "gpu_time_ms": g("gpu__time_duration.sum"),
+         "dram_bytes_read": rd * unit_scale if rd is not None else None,
+         "dram_bytes_write": wr * unit_scale if wr is not None else None,
+         "dram_bytes_per_launch": (rd + wr) * unit_scale if rd is not None and wr is not None else None,
+         "l2_hit_rate_pct": g("lts__t_sector_hit_rate.pct"),
+         "l1_data_pipe_lsu_wavefronts_pct": g("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+         "instructions": g("smsp__inst_executed.sum"),
+         "rows": nrows_}
+    with open(out_json, "w") as f:
+        _json.dump(d, f, indent=1)
+    return d
+
+
+if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "--write":
+    import os
+    write_summary(rep, sys.argv[4], "profiles/ncu_numeric_summary.json", sys.argv[5], nrows)
