@@ -112,6 +112,7 @@ struct ptap_plan {
   // plan-mapped numeric (all-at-once / merged)
   bool mapped = false;
   bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
+  bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool want_maps = false;
   MapArgs maps{};
   MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
@@ -244,6 +245,7 @@ int ceil_log2(unsigned long long v) {
 // ---- bins -------------------------------------------------------------------
 LaunchShape shape_for(int q, const BinSet &bs) {
   LaunchShape s{};
+  s.bin = q;
   s.gtables = nullptr;
   s.max_ctas = 148 * 64;
   switch (q) {
@@ -559,6 +561,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
     const int64_t nnz_max = std::max<int64_t>({ops->a_diag.nnz, ops->a_off.nnz, ops->p_diag.nnz, ops->p_off.nnz,
                                       ops->p_remote.nnz});
     p->q4 = h[1] <= 128 && p->nloc < lim && nnz_max < lim && !getenv("PTAP_NO_Q4");
+    p->q4_sym = p->q4 && !getenv("PTAP_NO_Q4_SYMBOLIC");
   }
   int64_t *slen = nullptr, *scratch = nullptr;
   CKS(palloc(p, &slen, p->nloc, CAT_TRANSIENT, st));
@@ -784,6 +787,8 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     BinSet &bs = merged ? p->bins_all : p->bins_send;
     auto pass = [&]() -> ptap_status {
       return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+        if (s.bin == 0 && p->q4_sym && p->mo.smap)
+          return launch_outer_symbolic_q4(op, rows, n, 1, merged ? 1 : 0, p->local_arena, send, p->mo, p->d_status, st);
         return launch_outer_symbolic(s, op, rows, n, 1, merged ? 1 : 0, p->local_arena, send, p->mo, p->d_status, st);
       });
     };
@@ -842,6 +847,8 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
     CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
       return for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
         Arena none{nullptr, 0};
+        if (s.bin == 0 && p->q4_sym && p->mo.smap)
+          return launch_outer_symbolic_q4(op, rows, n, 0, 1, la, none, p->mo, p->d_status, st);
         return launch_outer_symbolic(s, op, rows, n, 0, 1, la, none, p->mo, p->d_status, st);
       });
     }));

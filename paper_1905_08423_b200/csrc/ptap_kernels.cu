@@ -902,6 +902,220 @@ __global__ void k_arena_rehash(Arena from, Arena to, int *status) {
   if (k != EMPTY64) arena_insert(to, k / to.m, k % to.m, status);
 }
 
+// Bin-0 structural outer products with the slot maps (AP rows <= 32 slots,
+// <= 128 fold pairs per row, every offset within 32 bits -- the plan's q4
+// condition): 8 fine rows per warp, 4 lanes each, one 64-slot table per row.
+// A single walk over the pairs in fold order inserts the AP columns; the pair
+// that inserts a key is that key's first in fold order, so recording the
+// table position (and an inserted bit) per pair gives the slot map once the
+// row's pattern is ranked -- no second walk and no per-pair probe.  The map
+// bytes are assembled in shared memory and stored as aligned 32-bit words.
+constexpr int SQ_R = 8, SQ_G = 4, SQ_LOG2T = 6, SQ_T = 64, SQ_SMB = 132;
+struct SqWarp {
+  int32_t keys[SQ_R][SQ_T];
+  int32_t lk[SQ_R][SQ_T];       // compacted keys
+  uint8_t lpos[SQ_R][SQ_T];     // their table positions
+  uint8_t slot_of[SQ_R][SQ_T];  // table position -> slot (rank)
+  uint32_t sm[SQ_R][SQ_SMB / 4];  // slot bytes of the row, at (start & 3) + pair
+  int2 dp[SQ_G][SQ_R];          // step entries: P row start, packed offsets/lengths
+  int32_t o0[SQ_G][SQ_R];       // P_o row start of the step entry
+};
+
+template <int SRC>
+__device__ __forceinline__ void sq_walk(const Ops &op, SqWarp &W, int i, int gl, int r, int sbo, int &run) {
+  constexpr int G = SQ_G;
+  const int64_t *arp = SRC ? op.ao_rp : op.ad_rp;
+  const int32_t *acol = SRC ? op.ao_col : op.ad_col;
+  const int64_t *qrp = SRC ? op.pr_rp : op.pd_rp;
+  const int32_t *qcol = SRC ? op.pr_col : op.pd_col;
+  const int32_t coff = SRC ? 0 : (int32_t)op.c_lo;
+  const bool po_here = SRC == 0 && op.po_rp != nullptr;
+  int32_t *keys = W.keys[r];
+  uint8_t *smb = (uint8_t *)W.sm[r];
+  int t0 = 0, len = 0;
+  if (i >= 0) { t0 = (int)__ldg(arp + i); len = (int)__ldg(arp + i + 1) - t0; }
+  const int maxlen = __reduce_max_sync(FULL, len);
+#pragma unroll 1
+  for (int tb = 0; tb < maxlen; tb += G) {
+    const int t = tb + gl;
+    int d0 = 0, o0 = 0, nd = 0, plen = 0;
+    if (t < len) {
+      const int k = __ldg(acol + t0 + t);
+      d0 = (int)__ldg(qrp + k);
+      nd = plen = (int)__ldg(qrp + k + 1) - d0;
+      if (po_here) {
+        o0 = (int)__ldg(op.po_rp + k);
+        plen += (int)__ldg(op.po_rp + k + 1) - o0;
+      }
+    }
+    int incl = plen;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o, G);
+      if (gl >= o) incl += y;
+    }
+    W.dp[gl][r] = make_int2(d0, (int)((uint32_t)(run + incl - plen) | ((uint32_t)nd << 16) | ((uint32_t)plen << 24)));
+    if (po_here) W.o0[gl][r] = o0;
+    run += __shfl_sync(FULL, incl, G - 1, G);
+    __syncwarp();
+    const int steps = min(G, maxlen - tb);
+    // the AP columns of all steps first (independent loads), then the inserts
+    // in step order
+    int32_t gv[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      gv[j] = EMPTY32;
+      if (j < steps) {
+        const int2 e = W.dp[j][r];
+        const int plj = (int)((uint32_t)e.y >> 24), ndj = (e.y >> 16) & 0xff;
+        if (gl < plj)
+          gv[j] = gl < ndj ? __ldg(qcol + e.x + gl) + coff
+                           : op.p_colmap[op.po_col[W.o0[j][r] + (gl - ndj)]];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (j < steps) {
+        const int2 e = W.dp[j][r];
+        const int plj = (int)((uint32_t)e.y >> 24), ndj = (e.y >> 16) & 0xff, off = sbo + (e.y & 0xffff);
+        for (int u = gl; u < plj; u += G) {
+          const int32_t g = u == gl ? gv[j] : (u < ndj ? __ldg(qcol + e.x + u) + coff
+                                                       : op.p_colmap[op.po_col[W.o0[j][r] + (u - ndj)]]);
+          uint32_t h = hash32((uint32_t)g, SQ_LOG2T);
+          uint8_t rec = 0xff;
+          for (int probe = 0; probe < SQ_T; ++probe) {
+            const int32_t kk = keys[h];
+            if (kk == g) { rec = (uint8_t)h; break; }
+            if (kk == EMPTY32) {
+              const int32_t old = atomicCAS(keys + h, EMPTY32, g);
+              if (old == EMPTY32) { rec = (uint8_t)(h | 0x80); break; }
+              if (old == g) { rec = (uint8_t)h; break; }
+            }
+            h = (h + 1) & (SQ_T - 1);
+          }
+          smb[off + u] = rec;  // 0xff: table full (cannot happen for <= 32 keys)
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                           int do_send, int do_local, Arena local, Arena send,
+                                                           MapOut mo, int *status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int G = SQ_G;
+  const int lane = lane_id(), gl = lane & (G - 1), r = lane / G;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  SqWarp &W = ((SqWarp *)smem)[warp];
+  const int total = (int)nrows;
+  for (int r0 = (blockIdx.x * nwarps + warp) * SQ_R; r0 < total; r0 += gridDim.x * nwarps * SQ_R) {
+    const int ridx = r0 + r;
+    int i = ridx < total ? (rows ? rows[ridx] : ridx) : -1;
+    int pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
+    if (i >= 0) {
+      pd0 = (int)__ldg(op.pd_rp + i); pd1 = (int)__ldg(op.pd_rp + i + 1);
+      if (op.po_rp) { po0 = (int)__ldg(op.po_rp + i); po1 = (int)__ldg(op.po_rp + i + 1); }
+    }
+    const bool wl = do_local && pd1 > pd0, ws = do_send && po1 > po0;
+    if (!(wl || ws)) i = -1;
+    if (__all_sync(FULL, i < 0)) continue;
+    const int sb = i >= 0 ? (int)mo.smap_rp[i] : 0;
+    const int sbo = sb & 3;
+    for (int x = gl; x < SQ_T; x += G) W.keys[r][x] = EMPTY32;
+    __syncwarp();
+    int run = 0;
+    sq_walk<0>(op, W, i, gl, r, sbo, run);
+    if (op.ao_rp != nullptr) sq_walk<1>(op, W, i, gl, r, sbo, run);
+    // compact the row's keys with their table positions
+    int n = 0;
+    const unsigned gmask = 0xfu << (lane & ~(G - 1));
+    for (int s0 = 0; s0 < SQ_T; s0 += G) {
+      const int sidx = s0 + gl;
+      const int32_t k = W.keys[r][sidx];
+      const bool occ = k != EMPTY32;
+      const unsigned b = __ballot_sync(FULL, occ) & gmask;
+      if (occ) {
+        const int at = n + __popc(b & ((1u << lane) - 1u));
+        W.lk[r][at] = k;
+        W.lpos[r][at] = (uint8_t)sidx;
+      }
+      n += __popc(b);
+    }
+    __syncwarp();
+    // slot = rank of the key in the row (sorted pattern), no sort needed
+    if (i >= 0) {
+      int32_t *pat = mo.pat + mo.pat_rp[i];
+      for (int x = gl; x < n; x += G) {
+        const int32_t g = W.lk[r][x];
+        int rk = 0;
+        for (int y = 0; y < n; ++y) rk += W.lk[r][y] < g;
+        pat[rk] = g;
+        W.slot_of[r][W.lpos[r][x]] = (uint8_t)rk;
+      }
+      if (gl == 0) mo.nap[i] = (uint8_t)n;
+    }
+    __syncwarp();
+    // slot bytes: table position -> slot, keeping the first-product bit; then
+    // store them (aligned interior as 32-bit words, the two ends as bytes)
+    if (i >= 0) {
+      const int npairs = run;
+      uint8_t *smb = (uint8_t *)W.sm[r];
+      for (int q = gl; q < npairs; q += G) {
+        const uint8_t b = smb[sbo + q];
+        smb[sbo + q] = (uint8_t)(W.slot_of[r][b & 0x7f] | (b & 0x80));
+      }
+      __syncwarp(0xfu << (lane & ~(G - 1)));
+      uint8_t *dst = mo.smap + (int64_t)sb - sbo;  // 4-byte aligned
+      const int nbytes = sbo + npairs, nw = (nbytes + 3) >> 2;
+      for (int w = gl; w < nw; w += G) {
+        const bool edge = (w == 0 && sbo != 0) || (w == nw - 1 && (nbytes & 3) != 0);
+        if (!edge) {
+          ((uint32_t *)dst)[w] = W.sm[r][w];
+        } else {
+          for (int c = 0; c < 4; ++c) {
+            const int q = 4 * w + c;
+            if (q >= sbo && q < nbytes) dst[q] = smb[q];
+          }
+        }
+      }
+    }
+    // structural outer products into the arenas
+    if (i >= 0 && n > 0) {
+      if (wl)
+        for (int jj = pd0; jj < pd1; ++jj) {
+          const unsigned long long J = (unsigned long long)__ldg(op.pd_col + jj);
+          for (int e = gl; e < n; e += G) arena_insert(local, J, (unsigned long long)W.lk[r][e], status);
+        }
+      if (ws)
+        for (int jj = po0; jj < po1; ++jj) {
+          const unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[jj]];
+          for (int e = gl; e < n; e += G) arena_insert(send, J, (unsigned long long)W.lk[r][e], status);
+        }
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigned long long nrows, int do_send,
+                                     int do_local, Arena local, Arena send, const MapOut &mo, int *status,
+                                     cudaStream_t stream) {
+  if (nrows == 0) return cudaSuccess;
+  const int warps = 8;
+  const size_t sm = (size_t)warps * sizeof(SqWarp);
+  cudaError_t e;
+  if (sm > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(k_outer_symbolic_q4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+    return e;
+  const unsigned long long rpc = (unsigned long long)warps * SQ_R;
+  unsigned long long grid = (nrows + rpc - 1) / rpc;
+  grid = std::min<unsigned long long>(grid, 148ull * 64);
+  k_outer_symbolic_q4<<<(int)grid, warps * 32, sm, stream>>>(op, rows, nrows, do_send, do_local, local, send, mo,
+                                                             status);
+  return cudaGetLastError();
+}
+
 // exact table sizes for the two-step P^T C~ rows: the length of the target
 // row of the allocated structure (C row, or staging row when present)
 __global__ void k_ptc_est(int64_t nrows, const int32_t *target_map, int64_t target_offset, int is_staging,

@@ -60,6 +60,7 @@ struct MapArgs {
 };
 
 struct LaunchShape {
+  int bin;       // work bin of the rows
   int group;     // 8 or 32 lanes per row
   int warps;     // warps per CTA
   int log2t;     // table slots = 1 << log2t
@@ -78,6 +79,9 @@ cudaError_t launch_ap_count_small(const Ops &op, int64_t nrows, const int64_t *a
                                   cudaStream_t st);
 cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *apub, int64_t *est2,
                              unsigned long long *nretry, cudaStream_t st);
+cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigned long long nrows, int do_send,
+                                     int do_local, Arena local, Arena send, const MapOut &mo, int *status,
+                                     cudaStream_t stream);
 cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                             int64_t *ap_nnz, int *status, cudaStream_t stream);
 cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
