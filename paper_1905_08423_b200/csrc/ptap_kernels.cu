@@ -358,8 +358,12 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
 __global__ void __launch_bounds__(256) k_build_pmap(Ops op, unsigned long long nrows, MapArgs mp, MapOut mo,
                                                     OuterTargets tg, int *status) {
   constexpr int G = 8;
+  // the row's sorted AP pattern (<= 255 columns) is searched from shared memory
+  __shared__ int32_t spat_all[256 / G][256];
   const int gl = lane_id() & (G - 1);
   const int gpc = (blockDim.x >> 5) * (32 / G);
+  int32_t *pat = spat_all[threadIdx.x / G];
+  const unsigned gmask = 0xffu << (lane_id() & ~(G - 1));
   for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * (32 / G); r0 < nrows;
        r0 += (unsigned long long)gridDim.x * gpc) {
     unsigned long long ridx = r0 + lane_id() / G;
@@ -370,7 +374,10 @@ __global__ void __launch_bounds__(256) k_build_pmap(Ops op, unsigned long long n
     int ndP = (int)(pd1 - pd0), nP = ndP + (int)(po1 - po0);
     if (nP == 0) continue;
     int n = mp.nap[i];
-    const int32_t *pat = mo.pat + mo.pat_rp[i];
+    const int32_t *gpat = mo.pat + mo.pat_rp[i];
+    __syncwarp(gmask);
+    for (int x = gl; x < n; x += G) pat[x] = gpat[x];
+    __syncwarp(gmask);
     uint8_t *pm = mp.pmap + mp.pmap_rp[i];
     for (int jj = 0; jj < nP; ++jj) {
       int64_t c0, c1;
