@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--csv", default=None, help="also write the reference bench's CSV columns (src/bench.py:43-56) "
+                                                  "plus GFLOP/s, GB/s and roofline, one row per algorithm")
     return ap.parse_args()
 
 
@@ -258,6 +260,44 @@ def time_numeric(pk, a, p, plan, ctx, steps, warmup, torch, kernel_events=None):
     return total_ms / steps, kern, launches
 
 
+def row_scaled_diff(rp_a, val_a, rp_b, val_b, torch):
+    """max over entries of |a - b| / max_k |a_ik| (SURVEY §8(c) values B);
+    inf if the two patterns' row offsets differ."""
+    if rp_a.numel() != rp_b.numel() or not torch.equal(rp_a, rp_b):
+        return float("inf")
+    n = rp_a.numel() - 1
+    if val_a.numel() == 0:
+        return 0.0
+    rows = torch.repeat_interleave(torch.arange(n, device=rp_a.device), rp_a[1:] - rp_a[:-1])
+    scale = torch.zeros(n, dtype=torch.float64, device=rp_a.device)
+    scale.scatter_reduce_(0, rows, val_a.abs(), reduce="amax")
+    d = (val_a - val_b).abs() / scale[rows].clamp_min(1e-300)
+    return float(d.max().item())
+
+
+def write_csv(path, line, out, ctx):
+    """The reference bench's CSV columns (src/bench.py:43-56) plus this
+    bench's rates, one row per algorithm."""
+    import csv
+    cols = ["np", "algorithm", "mem_input", "mem_output", "mem_aux", "mem_transient_peak", "mem_plan",
+            "time_sym_s", "time_num_s", "time_total_s", "repeats", "verified",
+            "gflops", "alg_gbs", "roofline_frac", "n_gpus"]
+    mac2 = 2.0 * line["config"]["mac_total"]
+    alg_bytes = line["roofline"]["alg_bytes_per_launch"] * ctx.nranks
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(cols)
+        for alg, v in out.items():
+            mem = v["memory"]["peak"]
+            t_num = v["numeric_ms"] * 1e-3
+            diff = v.get("row_scaled_diff_vs_allatonce", 0.0)
+            w.writerow([ctx.nranks, alg, mem["input_matrices"], mem["output_matrix"], mem["auxiliary_matrices"],
+                        mem["transient_hash_peak"], mem["plan_cache"], v["symbolic_ms"] * 1e-3, t_num,
+                        v["symbolic_ms"] * 1e-3 + t_num, line["steps"], bool(diff <= 1e-12),
+                        mac2 / t_num / 1e9, alg_bytes / t_num / 1e9,
+                        alg_bytes / t_num / 1e9 / (line["roofline"]["peak"] * ctx.nranks), ctx.nranks])
+
+
 def max_over_ranks(x, ctx, torch):
     if ctx.nranks == 1:
         return x
@@ -374,6 +414,8 @@ def our_arm(args):
 
     # --- variants (headline plan released first so every variant's warm
     # symbolic phase sees the same memory pool state) -----------------------------
+    # the all-at-once C is kept to cross-check the variants on the device
+    c_rp_ref, c_val_ref = (c_rp.clone(), c_val.clone()) if not args.no_variants else (None, None)
     del plan, c_rp, c_col, c_val
     gc.collect()
     torch.cuda.synchronize()
@@ -383,14 +425,18 @@ def our_arm(args):
             vms, _, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
             vmem = vplan.memory()
             vms = max_over_ranks(vms, ctx, torch)
+            vrp, _, vval = vplan.c_device()
+            diff = max_over_ranks(row_scaled_diff(c_rp_ref, c_val_ref, vrp, vval, torch), ctx, torch)
             out[alg] = {"numeric_ms": vms, "symbolic_ms": vsym * 1e3, "symbolic_cold_ms": vcold * 1e3,
                         "symbolic_warm_runs_ms": [t * 1e3 for t in vall],
                         "ptap_wall_ms": vsym * 1e3 + vms,
                         "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
+                        "row_scaled_diff_vs_allatonce": diff,
                         "memory": vmem}
-            del vplan
+            del vplan, vrp, vval
             gc.collect()
             torch.cuda.synchronize()
+        del c_rp_ref, c_val_ref
 
     # --- CPU baseline (rank 0, N = 1) -----------------------------------------
     cpu = None
@@ -427,6 +473,8 @@ def our_arm(args):
         if "two-step" in out:
             line["variants"]["allatonce_over_two_step_time"] = out["allatonce"]["numeric_ms"] / out["two-step"]["numeric_ms"]
         print(json.dumps(line))
+        if args.csv:
+            write_csv(args.csv, line, out, ctx)
     if ctx.nranks > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
