@@ -15,6 +15,7 @@ from .ledger import MemoryLedger, PhaseTimer, PlanCounters
 from .partition import (DistMatrix, LocalMatrix, NeighborList, RowPartition, assemble_global,
                         build_neighbor_list, dist_from_global, make_partition, owner, split_local)
 from .hierarchy import GalerkinHierarchy, HierarchyLevel
+from .matio import load_npz, read_matrix_market, save_npz, write_matrix_market
 from .problems import model_problem_global, random_instance
 from .sparse import CsrMatrix, RowAccumulator, RowSet, Triplet, csr_from_triplets, relative_difference, transpose
 from .tripleproduct import (ALGORITHMS, ALL_AT_ONCE, CACHE_FREE, CACHE_KEEP, MERGED, TWO_STEP,
