@@ -15,6 +15,8 @@
  *   ptap_numeric_send                           numeric send loop           src/tripleproduct.py:303-341, 440-470
  *   ptap_numeric_local                          numeric local loop          src/tripleproduct.py:342-348, 472-486
  *   ptap_numeric_merge                          _merge_numeric_batches      src/tripleproduct.py:215-229
+ *   ptap_numeric_local_rows, ptap_plan_c_last_row  the local loop over a row  src/tripleproduct.py:342-348
+ *                                               range (streamed uploads)
  *   ptap_plan_release_cache                     release_cache (cache=free)  src/tripleproduct.py:127-139
  *   ptap_plan_memory                            MemoryLedger categories     src/ledger.py:23-34
  *   ptap_plan_counters                          PlanCounters                src/ledger.py:149-156
@@ -167,6 +169,17 @@ ptap_status ptap_symbolic_local(ptap_plan *plan, const ptap_operands *ops,
 ptap_status ptap_numeric_send(ptap_plan *plan, const ptap_operands *ops, void *stream);
 ptap_status ptap_numeric_local(ptap_plan *plan, const ptap_operands *ops, void *stream);
 ptap_status ptap_numeric_merge(ptap_plan *plan, const double *recv_vals, void *stream);
+/* All-at-once local loop over the fine rows [row_lo, row_hi) only, so a
+ * caller can fold row blocks as their A values arrive (flags bit 0: zero C
+ * first; bit 1: also run the rows outside the range-addressable bin -- pass
+ * it on the last block).  Returns PTAP_ERR_VALUE when the plan's local rows
+ * are not one range-addressable bin (callers then use ptap_numeric_local). */
+ptap_status ptap_numeric_local_rows(ptap_plan *plan, const ptap_operands *ops, int64_t row_lo, int64_t row_hi,
+                                    int flags, void *stream);
+/* last[J] (device, int32, one per local C row) = the largest local fine row
+ * contributing to C row J, -1 for none: C row J is final once rows <= last[J]
+ * are folded. */
+ptap_status ptap_plan_c_last_row(ptap_plan *plan, const ptap_operands *ops, int32_t *last, void *stream);
 /* Synchronise and report device-side drift detected by the last numeric pass. */
 ptap_status ptap_plan_check(ptap_plan *plan, void *stream);
 

@@ -278,7 +278,8 @@ ptap_status build_bins(ptap_plan *p, BinSet &bs, int64_t nrows, const int64_t *e
   CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   bs.selected = (int64_t)h[4];
-  bool identity = (mode == 0 && (int64_t)h[0] == nrows);
+  // every row selected and in bin 0: the bin is the identity list
+  bool identity = (int64_t)h[0] == nrows;
   if (identity) {
     bs.identity0 = true;
     bs.count[0] = nrows;
@@ -966,6 +967,32 @@ ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *str
     p->cnt.numeric_row_kernel_calls += p->bins_local.selected;
   }
   p->cnt.numeric_runs++;
+  return PTAP_OK;
+}
+
+ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int64_t row_lo, int64_t row_hi,
+                                    int flags, void *stream) {
+  CKS(numeric_ready(p));
+  if (p->alg != PTAP_ALLATONCE || !p->mapped || !p->q4 || !p->bins_local.identity0)
+    return fail(PTAP_ERR_VALUE, "plan has no range-addressable local rows");
+  if (row_lo < 0 || row_hi > p->nloc || row_lo > row_hi) return fail(PTAP_ERR_VALUE, "row range");
+  cudaStream_t st = (cudaStream_t)stream;
+  Ops op = make_ops(ops);
+  if ((flags & 1) && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
+  OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+  if (row_hi > row_lo) {
+    CK(launch_outer_numeric_mapped(3, op, nullptr, (unsigned long long)(row_hi - row_lo), p->maps, tg, 0, 1,
+                                   p->d_status, st, (int)row_lo));
+    p->cnt.kernel_launches++;
+    p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
+  }
+  if (flags & 2) p->cnt.numeric_runs++;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_c_last_row(ptap_plan *p, const ptap_operands *ops, int32_t *last, void *stream) {
+  CKS(numeric_ready(p));
+  CK(launch_c_last_row(p->nloc, ops->p_diag.row_ptr, ops->p_diag.col, p->ncl, last, (cudaStream_t)stream));
   return PTAP_OK;
 }
 

@@ -438,7 +438,7 @@ __device__ __forceinline__ void q4_fold(const Ops &op, Q4Warp &W, double *acc, c
 __global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_q4(Ops op, const int32_t *rows,
                                                                       unsigned long long nrows, MapArgs mp,
                                                                       OuterTargets tg, int do_send, int do_local,
-                                                                      int *status) {
+                                                                      int *status, int row0) {
   // 32-bit offsets throughout (the plan checks every array fits): 64-bit
   // live values would spill
   extern __shared__ __align__(16) unsigned char smem[];
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_q4(Ops op, con
   const int total = (int)nrows;
   for (int r0 = (blockIdx.x * nwarps + warp) * Q4_RPW; r0 < total; r0 += gridDim.x * nwarps * Q4_RPW) {
     const int ridx = r0 + r;
-    int i = ridx < total ? (rows ? rows[ridx] : ridx) : -1;
+    int i = ridx < total ? (rows ? rows[ridx] : row0 + ridx) : -1;
     const int i0 = __shfl_sync(FULL, i, 0);
     const bool contig = __all_sync(FULL, i >= 0 && i == i0 + r);
     bool wl = false, ws = false;
@@ -535,6 +535,23 @@ static unsigned long long resident(K kern, int threads, size_t smem) {
 
 static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 
+// last[J] = largest local fine row i with P_d(i, J) != 0 (-1: none): C row
+// J holds its final value once every fine row <= last[J] is folded
+__global__ void k_c_last_row(int64_t n, const int64_t *pd_rp, const int32_t *pd_col, int32_t *last) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t e = pd_rp[i]; e < pd_rp[i + 1]; ++e) atomicMax(last + pd_col[e], (int32_t)i);
+}
+
+cudaError_t launch_c_last_row(int64_t n, const int64_t *pd_rp, const int32_t *pd_col, int64_t ncl, int32_t *last,
+                              cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(last, 0xff, sizeof(int32_t) * (ncl > 0 ? ncl : 1), st);
+  if (e != cudaSuccess) return e;
+  if (n > 0) k_c_last_row<<<nb(n, 256), 256, 0, st>>>(n, pd_rp, pd_col, last);
+  return cudaGetLastError();
+}
+
+
 cudaError_t launch_map_lengths(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *apub,
                                const int64_t *ap_nnz, int64_t *slen, int64_t *plen, cudaStream_t st) {
   if (n > 0) k_map_lengths<<<nb(n, 256), 256, 0, st>>>(n, pd_rp, po_rp, apub, ap_nnz, slen, plen);
@@ -559,7 +576,7 @@ cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *
 
 cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                         const MapArgs &mp, const OuterTargets &tg, int do_send, int do_local,
-                                        int *status, cudaStream_t st) {
+                                        int *status, cudaStream_t st, int row0) {
   if (nrows == 0) return cudaSuccess;
   const int warps = 8;
   cudaError_t e;
@@ -569,7 +586,8 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
     const unsigned long long rpc = (unsigned long long)warps * Q4_RPW;
     unsigned long long grid = (nrows + rpc - 1) / rpc;
     grid = std::min(grid, grid_cap(k_outer_numeric_q4, warps * 32, sm));
-    k_outer_numeric_q4<<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local, status);
+    k_outer_numeric_q4<<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local, status,
+                                                          row0);
   } else if (bin == 0) {
     constexpr int G = 4, CAP = 32;
     const int gpc = warps * (32 / G);

@@ -386,11 +386,110 @@ def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str) ->
     return plan
 
 
+_UPLOAD_BLOCKS = 8  # row blocks of the streamed host-operand numeric pass (PTAP_UPLOAD_BLOCKS)
+
+
+def _streamable(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankContext) -> bool:
+    import os
+    if os.environ.get("PTAP_UPLOAD_BLOCKS", "") == "1" or getattr(plan, "_stream_ok", True) is False:
+        return False
+    return (ctx.nranks == 1 and plan.algorithm == ALL_AT_ONCE and isinstance(a.local, LocalMatrix)
+            and isinstance(p.local, LocalMatrix) and a.local.offdiag.nnz == 0 and p.local.offdiag.nnz == 0
+            and _torch().cuda.is_available())
+
+
+def _numeric_streamed(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankContext):
+    """All-at-once numeric pass at one rank with host operands, pipelined over
+    PCIe: P's values go up first, then A's values in row blocks on a copy
+    stream while the previous blocks fold (``ptap_numeric_local_rows``), and
+    C rows that are final (every contributing fine row folded, from the
+    plan's last-contributor map) come back on a third stream while later
+    blocks run.  Same kernels, same result as the one-shot path."""
+    import os
+
+    torch = _torch()
+    L = _lib.load()
+    # drift check as in _prepare
+    for which, m, tok in (("A", a, plan._a_token), ("P", p, plan._p_token)):
+        if tok is not None and _identity(m.local) != tok[0] and structure_token(m.local) != tok[1]:
+            raise StructuralDriftError(f"{which} changed structure since the symbolic phase")
+    st = plan._ops.struct()
+    dev = ctx.device
+    if getattr(plan, "_stream_state", None) is None:
+        up, dn = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        rp_d, _, val_d = plan.c_device()
+        last = torch.empty(max(rp_d.numel() - 1, 1), dtype=torch.int32, device=dev)
+        _lib.check(L.ptap_plan_c_last_row(plan._h, ctypes.byref(st), ctypes.c_void_p(last.data_ptr()),
+                                          _stream_ptr()), "last contributors")
+        pmax = np.maximum.accumulate(last[:rp_d.numel() - 1].cpu().numpy().astype(np.int64)) if rp_d.numel() > 1 \
+            else np.zeros(0, np.int64)
+        plan._stream_state = (up, dn, rp_d.cpu().numpy(), pmax)
+    up, dn, c_rp, pmax = plan._stream_state
+    nblk = max(1, int(os.environ.get("PTAP_UPLOAD_BLOCKS", _UPLOAD_BLOCKS)))
+    n = a.local.nrows
+    a_rp = a.local.diag.row_offsets
+    bounds = [n * k // nblk for k in range(nblk + 1)]
+    a_host = torch.from_numpy(a.local.diag.values)
+    p_host = torch.from_numpy(p.local.diag.values)
+    a_dev, p_dev = plan._a_dev.diag.val, plan._p_dev.diag.val
+    _, _, val_d = plan.c_device()
+    if getattr(plan, "_pinned_c", None) is None or plan._pinned_c.numel() != val_d.numel():
+        plan._pinned_c = torch.empty(val_d.numel(), dtype=torch.float64, pin_memory=True)
+    c_host = plan._pinned_c
+    comp = torch.cuda.current_stream(dev)
+    up.wait_stream(comp)  # the previous pass no longer reads the operands
+    dn.wait_stream(comp)
+    with ctx.timer.phase("numeric"):
+        with torch.cuda.stream(up):
+            p_dev.copy_(p_host, non_blocking=True)
+            ev_p = torch.cuda.Event()
+            ev_p.record(up)
+            ev_blk = []
+            for b in range(nblk):
+                lo, hi = int(a_rp[bounds[b]]), int(a_rp[bounds[b + 1]])
+                if hi > lo:
+                    a_dev[lo:hi].copy_(a_host[lo:hi], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(up)
+                ev_blk.append(e)
+        comp.wait_event(ev_p)
+        done_c = 0
+        for b in range(nblk):
+            comp.wait_event(ev_blk[b])
+            flags = (1 if b == 0 else 0) | (2 if b == nblk - 1 else 0)
+            status = L.ptap_numeric_local_rows(plan._h, ctypes.byref(st), bounds[b], bounds[b + 1], flags,
+                                               ctypes.c_void_p(comp.cuda_stream))
+            if status != 0 and b == 0:
+                plan._stream_ok = False  # not range-addressable: one-shot path from now on
+                return None
+            _lib.check(status, "numeric local rows")
+            # C rows whose last contributor has been folded
+            upto = int(np.searchsorted(pmax, bounds[b + 1], side="left")) if b < nblk - 1 else pmax.size
+            end = int(c_rp[upto]) if pmax.size else 0
+            if end > done_c:
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                dn.wait_event(ev)
+                with torch.cuda.stream(dn):
+                    c_host[done_c:end].copy_(val_d[done_c:end], non_blocking=True)
+                done_c = end
+        comp.wait_stream(dn)
+        _lib.check(L.ptap_plan_check(plan._h, _stream_ptr()), "numeric")
+    plan._sync_counters()
+    alloc = plan.c_alloc
+    alloc.local.diag.values = c_host.numpy()
+    return alloc.local
+
+
 def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankContext, expected: str,
              to_host: bool = True):
     if plan.algorithm != expected:
         raise ValueError(f"plan was built by {plan.algorithm!r}, not {expected!r}")
     plan._require_live()
+    if to_host and _streamable(a, p, plan, ctx):
+        local = _numeric_streamed(a, p, plan, ctx)
+        if local is not None:
+            return local
     L = _lib.load()
     with ctx.timer.phase("numeric"):
         _prepare(plan, a, p, ctx, symbolic=False)

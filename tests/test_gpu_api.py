@@ -173,3 +173,28 @@ def test_standalone_spgemm_matches_reference_golden():
         cols = sorted(acc)
         assert c.row_cols(i).tolist() == cols
         assert np.array_equal(np.array([acc[g] for g in cols]).view(np.uint64), c.row_values(i).view(np.uint64))
+
+
+def test_streamed_host_numeric_matches_one_shot():
+    """At one rank the all-at-once pass with host operands streams A's values
+    up in row blocks and final C rows back; the result equals the one-shot
+    path (same kernels) within the atomics' row-scaled 1e-15, for several
+    block counts, and numeric_runs counts passes, not blocks."""
+    A, P = _cfg3(20)
+    ctx = pk.single_rank_context()
+    a, p = pk.distribute(A, P, 1, 0)
+    plan = pk.run_symbolic(a, p, "allatonce", ctx)
+    os.environ["PTAP_UPLOAD_BLOCKS"] = "1"
+    try:
+        ref = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
+    finally:
+        del os.environ["PTAP_UPLOAD_BLOCKS"]
+    ip = plan.c_alloc.local.diag.row_offsets
+    for blocks in ("8", "3", "17"):
+        os.environ["PTAP_UPLOAD_BLOCKS"] = blocks
+        try:
+            got = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
+        finally:
+            del os.environ["PTAP_UPLOAD_BLOCKS"]
+        assert row_scaled_err(ip, got, ref) <= 1e-15
+    assert plan.counters.numeric_runs == 4
