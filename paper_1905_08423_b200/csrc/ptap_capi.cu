@@ -651,6 +651,65 @@ ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
   return PTAP_OK;
 }
 
+// C's structure without an arena (all-at-once, one rank): maps-only outer
+// pass over the local rows, P_d^T, then per C row the union of its
+// contributors' sorted AP rows (k_c_union).  PTAP_ERR_VALUE: some union did
+// not fit the per-row table (the caller then takes the arena path).
+ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st, Tracer *tr) {
+  Arena none{nullptr, 0};
+  CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+    if (s.bin == 0 && p->q4_sym && p->mo.smap)
+      return launch_outer_symbolic_q4(op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
+    return launch_outer_symbolic(s, op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
+  }));
+  p->cnt.symbolic_row_kernel_calls += p->bins_local.selected;
+  int s0 = 0;
+  CKS(read_status(p, st, &s0));
+  CKS(status_to_error(s0, "symbolic"));
+  tr->mark(st, "local outer symbolic (maps)");
+  // P_d^T structure: fine rows contributing to each local C row
+  const int64_t ncl = p->ncl, pnnz = ops->p_diag.nnz;
+  int64_t *cnt = nullptr, *t_rp = nullptr, *scratch = nullptr;
+  int32_t *t_row = nullptr;
+  CKS(palloc(p, &cnt, ncl, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ncl > 0 ? ncl : 1), st));
+  if (pnnz > 0) CK(launch_count_cols(pnnz, op.pd_col, cnt, st));
+  CKS(palloc(p, &t_rp, ncl + 1, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(ncl), CAT_TRANSIENT, st));
+  CK(scan_exclusive(cnt, t_rp, ncl, scratch, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ncl > 0 ? ncl : 1), st));
+  CKS(palloc(p, &t_row, pnnz, CAT_TRANSIENT, st));
+  CK(launch_transpose_scatter(p->nloc, op.pd_rp, op.pd_col, t_rp, cnt, t_row, nullptr, st));
+  tr->mark(st, "P_d^T");
+  // row sizes, then the rows
+  CK(launch_c_union(false, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, cnt, nullptr, nullptr,
+                    p->d_status, st));
+  int s1 = 0;
+  CKS(read_status(p, st, &s1));
+  ptap_status ret = PTAP_OK;
+  if (s1 & ST_TABLE_FULL) {
+    ret = PTAP_ERR_VALUE;
+  } else {
+    CKS(palloc(p, &p->c_rp, ncl + 1, CAT_OUTPUT, st));
+    CK(scan_exclusive(cnt, p->c_rp, ncl, scratch, st));
+    int64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, p->c_rp + ncl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    p->c_nnz = nnz;
+    CKS(palloc(p, &p->c_col, nnz, CAT_OUTPUT, st));
+    CK(launch_c_union(true, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, nullptr, p->c_rp, p->c_col,
+                      p->d_status, st));
+    p->cnt.kernel_launches += 2;
+  }
+  p->cnt.kernel_launches += 4;
+  pfree(p, cnt, st);
+  pfree(p, t_rp, st);
+  pfree(p, scratch, st);
+  pfree(p, t_row, st);
+  tr->mark(st, "C rows by unions");
+  return ret;
+}
+
 ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_send, int do_local, cudaStream_t st) {
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   if (p->mapped) {
@@ -840,9 +899,19 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   Ops op = make_ops(ops);
   int64_t rnnz = recv ? recv->nnz : 0;
   Tracer tr;
+  // one rank's structure only (nothing received): C row by row as unions of
+  // the contributors' AP rows, no global arena
+  bool use_union = p->alg == PTAP_ALLATONCE && p->want_maps && !(recv && recv->nrows > 0) &&
+                   !getenv("PTAP_NO_UNION");
+  if (use_union) {
+    ptap_status us = c_by_unions(p, op, ops, st, &tr);
+    if (us == PTAP_OK) goto c_allocated;
+    if (us != PTAP_ERR_VALUE) return us;  // PTAP_ERR_VALUE: a union outgrew the table -> arena path
+  }
   if (p->alg != PTAP_MERGED)
     CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st, (unsigned long long)p->ncl));
   tr.mark(st, "local arena alloc");
+  {
   Arena &la = p->local_arena;
   if (p->alg == PTAP_ALLATONCE) {
     CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
@@ -880,6 +949,8 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   tr.mark(st, "C drain + sort");
   pfree(p, la.keys, st);
   la = Arena{nullptr, 0};
+  }
+c_allocated:
   CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
   CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
   if (recv && recv->nrows > 0) {

@@ -337,12 +337,12 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
                                mo.smap + (i >= 0 ? mo.smap_rp[i] : 0), n <= 127);
     }
     if (i >= 0 && n > 0) {
-      if (wl)
+      if (wl && local.keys)
         for (int64_t jj = pd0; jj < pd1; ++jj) {
           const unsigned long long J = (unsigned long long)__ldg(op.pd_col + jj);
           for (int e = gl; e < n; e += GROUP) arena_insert(local, J, (unsigned long long)tb.lk[e], status);
         }
-      if (ws)
+      if (ws && send.keys)
         for (int64_t jj = po0; jj < po1; ++jj) {
           const unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[jj]];
           for (int e = gl; e < n; e += GROUP) arena_insert(send, J, (unsigned long long)tb.lk[e], status);
@@ -693,7 +693,7 @@ __global__ void k_transpose_scatter(int64_t nrows, const int64_t *rp, const int3
     int32_t q = col[e];
     int64_t pos = t_rp[q] + (int64_t)atomicAdd((unsigned long long *)(cursor + q), 1ull);
     t_row[pos] = (int32_t)i;
-    t_perm[pos] = e;
+    if (t_perm) t_perm[pos] = e;
   }
 }
 
@@ -1090,12 +1090,12 @@ __global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t
     }
     // structural outer products into the arenas
     if (i >= 0 && n > 0) {
-      if (wl)
+      if (wl && local.keys)
         for (int jj = pd0; jj < pd1; ++jj) {
           const unsigned long long J = (unsigned long long)__ldg(op.pd_col + jj);
           for (int e = gl; e < n; e += G) arena_insert(local, J, (unsigned long long)W.lk[r][e], status);
         }
-      if (ws)
+      if (ws && send.keys)
         for (int jj = po0; jj < po1; ++jj) {
           const unsigned long long J = (unsigned long long)op.p_colmap[op.po_col[jj]];
           for (int e = gl; e < n; e += G) arena_insert(send, J, (unsigned long long)W.lk[r][e], status);
@@ -1120,6 +1120,112 @@ cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigne
   grid = std::min<unsigned long long>(grid, 148ull * 64);
   k_outer_symbolic_q4<<<(int)grid, warps * 32, sm, stream>>>(op, rows, nrows, do_send, do_local, local, send, mo,
                                                              status);
+  return cudaGetLastError();
+}
+
+// C's pattern row by row (one rank, nothing received): C(J,:) is the union of
+// the AP rows of the fine rows i with P_d(i,J) != 0 -- a per-row hash set in
+// shared memory, one warp per C row, instead of ~13 global-arena inserts per
+// entry (SURVEY §8(a) a6/a7 restated row-wise).  FILL = false counts (and
+// flags rows whose union does not fit the table), FILL = true writes the
+// sorted columns.
+constexpr int CU_LOG2T = 8, CU_T = 1 << CU_LOG2T, CU_MAX = 192;
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_rp, const int32_t *t_row,
+                                                 const int64_t *pat_rp, const int32_t *pat, const uint8_t *nap,
+                                                 int64_t *cnt, const int64_t *c_rp, int32_t *c_col, int *status) {
+  __shared__ int32_t keys_all[8][CU_T];
+  __shared__ int32_t lk_all[8][CU_T];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  int32_t *keys = keys_all[warp], *lk = lk_all[warp];
+  for (int64_t J = (int64_t)blockIdx.x * 8 + warp; J < ncl; J += (int64_t)gridDim.x * 8) {
+    for (int x = lane; x < CU_T; x += 32) keys[x] = EMPTY32;
+    __syncwarp();
+    bool full = false;
+    // contributors 32 at a time; their AP rows flattened over the lanes
+    for (int64_t tb = t_rp[J]; tb < t_rp[J + 1]; tb += 32) {
+      const int nc = (int)min((int64_t)32, t_rp[J + 1] - tb);
+      int my_n = 0;
+      int64_t my_base = 0;
+      if (lane < nc) {
+        const int32_t i = t_row[tb + lane];
+        my_n = nap[i];
+        my_base = pat_rp[i];
+      }
+      int incl = my_n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int tot = __shfl_sync(FULL, incl, 31);
+      const int excl = incl - my_n;
+      for (int q0 = 0; q0 < tot; q0 += 32) {
+        const int q = q0 + lane;
+        // contributor c holding flattened entry q: the last c with excl_c <= q
+        int c = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int cand = c + step;
+          const int ex = __shfl_sync(FULL, excl, cand < 32 ? cand : 31);
+          if (cand < nc && ex <= q) c = cand;
+        }
+        const int64_t base = __shfl_sync(FULL, my_base, c);
+        const int exc = __shfl_sync(FULL, excl, c);
+        if (q >= tot) continue;
+        const int32_t g = __ldg(pat + base + (q - exc));
+        uint32_t h = hash32((uint32_t)g, CU_LOG2T);
+        int probe = 0;
+        for (; probe < CU_T; ++probe) {
+          const int32_t k = keys[h];
+          if (k == g) break;
+          if (k == EMPTY32) {
+            const int32_t old = atomicCAS(keys + h, EMPTY32, g);
+            if (old == EMPTY32 || old == g) break;
+          }
+          h = (h + 1) & (CU_T - 1);
+        }
+        full |= probe == CU_T;
+      }
+    }
+    __syncwarp();
+    // compact
+    int n = 0;
+    for (int s0 = 0; s0 < CU_T; s0 += 32) {
+      const int32_t k = keys[s0 + lane];
+      const unsigned b = __ballot_sync(FULL, k != EMPTY32);
+      if (k != EMPTY32) lk[n + __popc(b & ((1u << lane) - 1u))] = k;
+      n += __popc(b);
+    }
+    __syncwarp();
+    full = __any_sync(FULL, full) || n > CU_MAX;
+    if (!FILL) {
+      if (lane == 0) {
+        cnt[J] = n;
+        if (full) atomicOr(status, ST_TABLE_FULL);
+      }
+    } else {
+      int32_t *out = c_col + c_rp[J];
+      for (int x = lane; x < n; x += 32) {
+        const int32_t g = lk[x];
+        int rk = 0;
+        for (int y = 0; y < n; ++y) rk += lk[y] < g;
+        out[rk] = g;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_c_union(bool fill, int64_t ncl, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
+                           const int32_t *pat, const uint8_t *nap, int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
+                           int *status, cudaStream_t st) {
+  if (ncl <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((ncl + 7) / 8, 148 * 16);
+  if (fill)
+    k_c_union<true><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, status);
+  else
+    k_c_union<false><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, status);
   return cudaGetLastError();
 }
 

@@ -82,6 +82,9 @@ cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *ap
 cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigned long long nrows, int do_send,
                                      int do_local, Arena local, Arena send, const MapOut &mo, int *status,
                                      cudaStream_t stream);
+cudaError_t launch_c_union(bool fill, int64_t ncl, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
+                           const int32_t *pat, const uint8_t *nap, int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
+                           int *status, cudaStream_t st);
 cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                             int64_t *ap_nnz, int *status, cudaStream_t stream);
 cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
