@@ -65,3 +65,38 @@ def test_bench_configs_match_oracle_small():
         if alg == "two-step":
             assert np.array_equal(c.values.view(np.uint64), want.val.view(np.uint64))
         assert row_scaled_err(want.row_ptr, c.values, want.val) <= TOL
+
+
+MANY_RANKS = [("toy", 3), ("dense_random_s4", 5), ("dense_random_s4", 8), ("random_instance_s11", 7),
+              ("random27_16", 4), ("poisson7_16", 4)]
+
+
+@pytest.mark.parametrize("case,nr", MANY_RANKS)
+def test_golden_parity_many_ranks(case, nr):
+    """Rank counts beyond 2 (uneven blocks, ranks owning one or two coarse
+    rows, several neighbours): all three algorithms in one launch of nr ranks
+    against the reference's own outputs at that np."""
+    import paper_1905_08423_b200 as pk
+    n, m, a, p, results = load_golden(case)
+    A = csr_from_arrays(n, n, *a)
+    P = csr_from_arrays(n, m, *p)
+
+    def prog(ctx):
+        aa, pp = pk.distribute(A, P, ctx.nranks, ctx.rank)
+        out = {}
+        for alg in ("two-step", "allatonce", "merged"):
+            c, _ = pk.ptap(aa, pp, alg, ctx)
+            out[alg] = c.local
+        return out
+
+    res = pk.spawn_ranks(nr, prog)
+    for alg in ("two-step", "allatonce", "merged"):
+        if (nr, alg) not in results:
+            continue
+        c = pk.assemble_global([r[alg] for r in res], ncols=P.ncols)
+        ip, j, v = results[(nr, alg)]
+        assert np.array_equal(c.row_offsets, ip) and np.array_equal(c.col_indices, j), (alg, "pattern")
+        if alg == "two-step" or case in DYADIC:
+            assert np.array_equal(c.values.view(np.uint64), v.view(np.uint64)), (alg, "bit-exact")
+        else:
+            assert row_scaled_err(ip, c.values, v) <= TOL, alg
