@@ -113,6 +113,7 @@ struct ptap_plan {
   bool mapped = false;
   bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
+  bool pmap_ready = false;          // position maps written by the row-union pass
   bool want_maps = false;
   MapArgs maps{};
   MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
@@ -593,12 +594,8 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   return PTAP_OK;
 }
 
-// Part 2 (C and the staging allocated): position maps, then drop the
-// transient patterns.  Falls back to the hash path if a target row is wider
-// than a byte can address.
-ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
-  p->mapped = false;
-  if (!p->want_maps) return PTAP_OK;
+// position-map storage (C rows and staging rows must fit a byte)
+ptap_status alloc_pmap(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st, bool *ok_out) {
   unsigned long long *mx = p->d_u64 + 12;
   CK(cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), st));
   CK(launch_max_rowlen(p->ncl, p->c_rp, mx, st));
@@ -606,32 +603,47 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   unsigned long long h[2];
   CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  bool ok = h[0] <= 256 && h[1] <= 256;
-  if (ok) {
-    int64_t *plen = nullptr, *scratch = nullptr, *unused = nullptr;
-    CKS(palloc(p, &plen, p->nloc, CAT_TRANSIENT, st));
-    CKS(palloc(p, &unused, p->nloc, CAT_TRANSIENT, st));
-    CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
-    CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, unused, plen, st));
-    CKS(palloc(p, &p->maps.pmap_rp, p->nloc + 1, CAT_PLAN, st));
-    CK(scan_exclusive(plen, p->maps.pmap_rp, p->nloc, scratch, st));
-    int64_t tot = 0;
-    CK(cudaMemcpyAsync(&tot, p->maps.pmap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    pfree(p, plen, st);
-    pfree(p, unused, st);
-    pfree(p, scratch, st);
-    p->pmap_bytes = tot;
-    CKS(palloc(p, &p->maps.pmap, tot, CAT_PLAN, st));
-    int64_t po_nnz = ops->p_off.nnz;
-    CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
-    if (po_nnz > 0)
-      CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
-    OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
-    CK(launch_build_pmap(op, (unsigned long long)p->nloc, p->maps, p->mo, tg, p->d_status, st));
-    p->cnt.kernel_launches += 5;
-    p->mapped = true;
+  *ok_out = h[0] <= 256 && h[1] <= 256;
+  if (!*ok_out) return PTAP_OK;
+  int64_t *plen = nullptr, *scratch = nullptr, *unused = nullptr;
+  CKS(palloc(p, &plen, p->nloc, CAT_TRANSIENT, st));
+  CKS(palloc(p, &unused, p->nloc, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(p->nloc), CAT_TRANSIENT, st));
+  CK(launch_map_lengths(p->nloc, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, unused, plen, st));
+  CKS(palloc(p, &p->maps.pmap_rp, p->nloc + 1, CAT_PLAN, st));
+  CK(scan_exclusive(plen, p->maps.pmap_rp, p->nloc, scratch, st));
+  int64_t tot = 0;
+  CK(cudaMemcpyAsync(&tot, p->maps.pmap_rp + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  pfree(p, plen, st);
+  pfree(p, unused, st);
+  pfree(p, scratch, st);
+  p->pmap_bytes = tot;
+  CKS(palloc(p, &p->maps.pmap, tot, CAT_PLAN, st));
+  int64_t po_nnz = ops->p_off.nnz;
+  CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
+  if (po_nnz > 0)
+    CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
+  p->cnt.kernel_launches += 4;
+  return PTAP_OK;
+}
+
+// Part 2 (C and the staging allocated): position maps (unless the row-union
+// pass already wrote them), then drop the transient patterns.  Falls back to
+// the hash path if a target row is wider than a byte can address.
+ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  p->mapped = false;
+  if (!p->want_maps) return PTAP_OK;
+  bool ok = p->pmap_ready;
+  if (!ok) {
+    CKS(alloc_pmap(p, op, ops, st, &ok));
+    if (ok) {
+      OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
+      CK(launch_build_pmap(op, (unsigned long long)p->nloc, p->maps, p->mo, tg, p->d_status, st));
+      p->cnt.kernel_launches++;
+    }
   }
+  p->mapped = ok;
   pfree(p, p->pat, st);
   pfree(p, p->pat_rp, st);
   p->mo = MapOut{};
@@ -682,8 +694,8 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
   CK(launch_transpose_scatter(p->nloc, op.pd_rp, op.pd_col, t_rp, cnt, t_row, nullptr, st));
   tr->mark(st, "P_d^T");
   // row sizes, then the rows
-  CK(launch_c_union(false, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, cnt, nullptr, nullptr,
-                    p->d_status, st));
+  CK(launch_c_union(false, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, cnt, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, nullptr, p->d_status, st));
   int s1 = 0;
   CKS(read_status(p, st, &s1));
   ptap_status ret = PTAP_OK;
@@ -697,8 +709,12 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
     CK(cudaStreamSynchronize(st));
     p->c_nnz = nnz;
     CKS(palloc(p, &p->c_col, nnz, CAT_OUTPUT, st));
+    bool pm_ok = false;
+    CKS(alloc_pmap(p, op, ops, st, &pm_ok));
     CK(launch_c_union(true, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, nullptr, p->c_rp, p->c_col,
+                      op.pd_rp, op.pd_col, pm_ok ? p->maps.pmap_rp : nullptr, pm_ok ? p->maps.pmap : nullptr,
                       p->d_status, st));
+    p->pmap_ready = pm_ok;
     p->cnt.kernel_launches += 2;
   }
   p->cnt.kernel_launches += 4;
@@ -899,10 +915,10 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   Ops op = make_ops(ops);
   int64_t rnnz = recv ? recv->nnz : 0;
   Tracer tr;
-  // one rank's structure only (nothing received): C row by row as unions of
-  // the contributors' AP rows, no global arena
+  // nothing received and nothing sent (every target row local): C row by
+  // row as unions of the contributors' AP rows, no global arena
   bool use_union = p->alg == PTAP_ALLATONCE && p->want_maps && !(recv && recv->nrows > 0) &&
-                   !getenv("PTAP_NO_UNION");
+                   ops->p_off.nnz == 0 && !getenv("PTAP_NO_UNION");
   if (use_union) {
     ptap_status us = c_by_unions(p, op, ops, st, &tr);
     if (us == PTAP_OK) goto c_allocated;

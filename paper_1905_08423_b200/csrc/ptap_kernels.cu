@@ -1130,71 +1130,105 @@ cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigne
 // flags rows whose union does not fit the table), FILL = true writes the
 // sorted columns.
 constexpr int CU_LOG2T = 8, CU_T = 1 << CU_LOG2T, CU_MAX = 192;
+
+// the contributors' AP entries of C row J, flattened over the warp's lanes
+// 32 contributors at a time; f(g, c_base_pm, s) is called for every entry
+// (g = column, s = its slot in the contributor's AP row)
+template <typename F>
+__device__ __forceinline__ void cu_sweep(int64_t J, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
+                                         const int32_t *pat, const uint8_t *nap, const int64_t *pd_rp,
+                                         const int32_t *pd_col, const int64_t *pmap_rp, F f) {
+  const int lane = lane_id();
+  for (int64_t tb = t_rp[J]; tb < t_rp[J + 1]; tb += 32) {
+    const int nc = (int)min((int64_t)32, t_rp[J + 1] - tb);
+    int my_n = 0;
+    int64_t my_base = 0, my_pm = -1;
+    if (lane < nc) {
+      const int32_t i = t_row[tb + lane];
+      my_n = nap[i];
+      my_base = pat_rp[i];
+      if (pmap_rp) {  // where row i's positions for target J go: jj-th block of its map
+        const int64_t e0 = pd_rp[i], e1 = pd_rp[i + 1];
+        int64_t jj = 0;
+        for (int64_t e = e0; e < e1; ++e)
+          if (pd_col[e] == (int32_t)J) { jj = e - e0; break; }
+        my_pm = pmap_rp[i] + jj * my_n;
+      }
+    }
+    int incl = my_n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int tot = __shfl_sync(FULL, incl, 31);
+    const int excl = incl - my_n;
+    for (int q0 = 0; q0 < tot; q0 += 32) {
+      const int q = q0 + lane;
+      int c = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = c + step;
+        const int ex = __shfl_sync(FULL, excl, cand < 32 ? cand : 31);
+        if (cand < nc && ex <= q) c = cand;
+      }
+      const int64_t base = __shfl_sync(FULL, my_base, c);
+      const int64_t pm = __shfl_sync(FULL, my_pm, c);
+      const int exc = __shfl_sync(FULL, excl, c);
+      if (q < tot) f(__ldg(pat + base + (q - exc)), pm, q - exc);
+    }
+  }
+}
+
+// C's pattern row by row (one rank, nothing received): C(J,:) is the union of
+// the AP rows of the fine rows i with P_d(i,J) != 0 -- a per-row hash set in
+// shared memory, one warp per C row, instead of ~13 global-arena inserts per
+// entry (SURVEY §8(a) a6/a7 restated row-wise).  FILL = false counts (and
+// flags rows whose union does not fit the table), FILL = true writes the
+// sorted columns and, when pmap is given, the position map of every
+// contributor (the byte position of each of its AP slots in C row J).
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_rp, const int32_t *t_row,
                                                  const int64_t *pat_rp, const int32_t *pat, const uint8_t *nap,
-                                                 int64_t *cnt, const int64_t *c_rp, int32_t *c_col, int *status) {
+                                                 int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
+                                                 const int64_t *pd_rp, const int32_t *pd_col,
+                                                 const int64_t *pmap_rp, uint8_t *pmap, int *status) {
   __shared__ int32_t keys_all[8][CU_T];
   __shared__ int32_t lk_all[8][CU_T];
+  __shared__ uint8_t lpos_all[8][CU_T];
+  __shared__ uint8_t rank_all[8][CU_T];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   int32_t *keys = keys_all[warp], *lk = lk_all[warp];
+  uint8_t *lpos = lpos_all[warp], *srank = rank_all[warp];
   for (int64_t J = (int64_t)blockIdx.x * 8 + warp; J < ncl; J += (int64_t)gridDim.x * 8) {
     for (int x = lane; x < CU_T; x += 32) keys[x] = EMPTY32;
     __syncwarp();
     bool full = false;
-    // contributors 32 at a time; their AP rows flattened over the lanes
-    for (int64_t tb = t_rp[J]; tb < t_rp[J + 1]; tb += 32) {
-      const int nc = (int)min((int64_t)32, t_rp[J + 1] - tb);
-      int my_n = 0;
-      int64_t my_base = 0;
-      if (lane < nc) {
-        const int32_t i = t_row[tb + lane];
-        my_n = nap[i];
-        my_base = pat_rp[i];
-      }
-      int incl = my_n;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int tot = __shfl_sync(FULL, incl, 31);
-      const int excl = incl - my_n;
-      for (int q0 = 0; q0 < tot; q0 += 32) {
-        const int q = q0 + lane;
-        // contributor c holding flattened entry q: the last c with excl_c <= q
-        int c = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int cand = c + step;
-          const int ex = __shfl_sync(FULL, excl, cand < 32 ? cand : 31);
-          if (cand < nc && ex <= q) c = cand;
+    cu_sweep(J, t_rp, t_row, pat_rp, pat, nap, nullptr, nullptr, nullptr, [&](int32_t g, int64_t, int) {
+      uint32_t h = hash32((uint32_t)g, CU_LOG2T);
+      int probe = 0;
+      for (; probe < CU_T; ++probe) {
+        const int32_t k = keys[h];
+        if (k == g) break;
+        if (k == EMPTY32) {
+          const int32_t old = atomicCAS(keys + h, EMPTY32, g);
+          if (old == EMPTY32 || old == g) break;
         }
-        const int64_t base = __shfl_sync(FULL, my_base, c);
-        const int exc = __shfl_sync(FULL, excl, c);
-        if (q >= tot) continue;
-        const int32_t g = __ldg(pat + base + (q - exc));
-        uint32_t h = hash32((uint32_t)g, CU_LOG2T);
-        int probe = 0;
-        for (; probe < CU_T; ++probe) {
-          const int32_t k = keys[h];
-          if (k == g) break;
-          if (k == EMPTY32) {
-            const int32_t old = atomicCAS(keys + h, EMPTY32, g);
-            if (old == EMPTY32 || old == g) break;
-          }
-          h = (h + 1) & (CU_T - 1);
-        }
-        full |= probe == CU_T;
+        h = (h + 1) & (CU_T - 1);
       }
-    }
+      full |= probe == CU_T;
+    });
     __syncwarp();
     // compact
     int n = 0;
     for (int s0 = 0; s0 < CU_T; s0 += 32) {
       const int32_t k = keys[s0 + lane];
       const unsigned b = __ballot_sync(FULL, k != EMPTY32);
-      if (k != EMPTY32) lk[n + __popc(b & ((1u << lane) - 1u))] = k;
+      if (k != EMPTY32) {
+        const int at = n + __popc(b & ((1u << lane) - 1u));
+        lk[at] = k;
+        lpos[at] = (uint8_t)(s0 + lane);
+      }
       n += __popc(b);
     }
     __syncwarp();
@@ -1211,7 +1245,15 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
         int rk = 0;
         for (int y = 0; y < n; ++y) rk += lk[y] < g;
         out[rk] = g;
+        srank[lpos[x]] = (uint8_t)rk;
       }
+      __syncwarp();
+      if (pmap)
+        cu_sweep(J, t_rp, t_row, pat_rp, pat, nap, pd_rp, pd_col, pmap_rp, [&](int32_t g, int64_t pm, int sl) {
+          uint32_t h = hash32((uint32_t)g, CU_LOG2T);
+          for (int probe = 0; probe < CU_T && keys[h] != g; ++probe) h = (h + 1) & (CU_T - 1);
+          pmap[pm + sl] = srank[h];
+        });
     }
     __syncwarp();
   }
@@ -1219,13 +1261,16 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
 
 cudaError_t launch_c_union(bool fill, int64_t ncl, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
                            const int32_t *pat, const uint8_t *nap, int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
+                           const int64_t *pd_rp, const int32_t *pd_col, const int64_t *pmap_rp, uint8_t *pmap,
                            int *status, cudaStream_t st) {
   if (ncl <= 0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>((ncl + 7) / 8, 148 * 16);
   if (fill)
-    k_c_union<true><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, status);
+    k_c_union<true><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, pd_rp, pd_col,
+                                          pmap_rp, pmap, status);
   else
-    k_c_union<false><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, status);
+    k_c_union<false><<<grid, 256, 0, st>>>(ncl, t_rp, t_row, pat_rp, pat, nap, cnt, c_rp, c_col, pd_rp, pd_col,
+                                           pmap_rp, pmap, status);
   return cudaGetLastError();
 }
 

@@ -84,6 +84,7 @@ cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigne
                                      cudaStream_t stream);
 cudaError_t launch_c_union(bool fill, int64_t ncl, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
                            const int32_t *pat, const uint8_t *nap, int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
+                           const int64_t *pd_rp, const int32_t *pd_col, const int64_t *pmap_rp, uint8_t *pmap,
                            int *status, cudaStream_t st);
 cudaError_t launch_ap_count(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                             int64_t *ap_nnz, int *status, cudaStream_t stream);
