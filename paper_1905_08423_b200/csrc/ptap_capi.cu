@@ -114,6 +114,7 @@ struct ptap_plan {
   bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool pmap_ready = false;          // position maps written by the row-union pass
+  bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
   bool want_maps = false;
   MapArgs maps{};
   MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
@@ -849,7 +850,14 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     p->cnt.symbolic_row_kernel_calls += p->nloc;
   } else {
     bool merged = p->alg == PTAP_MERGED;
-    if (merged) {
+    // merged with nothing to send: the fused loop is the local loop, whose
+    // structure is then built in symbolic_local exactly as for all-at-once
+    p->merged_deferred = merged && ops->p_off.nnz == 0 && !getenv("PTAP_NO_UNION");
+    if (p->merged_deferred) {
+      CKS(build_bins(p, p->bins_all, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 3, true, CAT_PLAN, st));
+      CKS(build_bins(p, p->bins_local, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 2, true, CAT_PLAN, st));
+      merged = false;  // the send pass below has no rows
+    } else if (merged) {
       CKS(build_bins(p, p->bins_all, p->nloc, p->ap_nnz, op.pd_rp, op.po_rp, 3, true, CAT_PLAN, st));
       p->cnt.symbolic_row_kernel_calls += p->bins_all.selected;
     } else {
@@ -860,7 +868,8 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
     Arena send{nullptr, 0};
     CKS(arena_alloc(p, send, p->bound_send + 16, st));
     if (merged) CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, 0), st, (unsigned long long)p->ncl));
-    BinSet &bs = merged ? p->bins_all : p->bins_send;
+    BinSet empty_bins{};
+    BinSet &bs = merged ? p->bins_all : (p->merged_deferred ? empty_bins : p->bins_send);
     auto pass = [&]() -> ptap_status {
       return for_bins(p, bs, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
         if (s.bin == 0 && p->q4_sym && p->mo.smap)
@@ -917,19 +926,20 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   Tracer tr;
   // nothing received and nothing sent (every target row local): C row by
   // row as unions of the contributors' AP rows, no global arena
-  bool use_union = p->alg == PTAP_ALLATONCE && p->want_maps && !(recv && recv->nrows > 0) &&
-                   ops->p_off.nnz == 0 && !getenv("PTAP_NO_UNION");
+  const bool local_loop_here = p->alg == PTAP_ALLATONCE || p->merged_deferred;
+  bool use_union = local_loop_here && p->want_maps && !(recv && recv->nrows > 0) && ops->p_off.nnz == 0 &&
+                   !getenv("PTAP_NO_UNION");
   if (use_union) {
     ptap_status us = c_by_unions(p, op, ops, st, &tr);
     if (us == PTAP_OK) goto c_allocated;
     if (us != PTAP_ERR_VALUE) return us;  // PTAP_ERR_VALUE: a union outgrew the table -> arena path
   }
-  if (p->alg != PTAP_MERGED)
+  if (p->alg != PTAP_MERGED || p->merged_deferred)
     CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st, (unsigned long long)p->ncl));
   tr.mark(st, "local arena alloc");
   {
   Arena &la = p->local_arena;
-  if (p->alg == PTAP_ALLATONCE) {
+  if (local_loop_here) {
     CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
       return for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
         Arena none{nullptr, 0};

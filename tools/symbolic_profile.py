@@ -11,11 +11,12 @@ import torch
 import paper_1905_08423_b200 as pk
 from paper_1905_08423_b200 import devgen
 
+ALG = sys.argv[1] if len(sys.argv) > 1 else "allatonce"
 ctx = pk.single_rank_context()
 a, p = devgen.config_dist('cfg3', 1, 0, ctx.device)
 torch.cuda.synchronize()
 for _ in range(2):
-    plan = pk.run_symbolic(a, p, "allatonce", ctx)
+    plan = pk.run_symbolic(a, p, ALG, ctx)
     del plan
     gc.collect()
 torch.cuda.synchronize()
@@ -23,7 +24,7 @@ pr = cProfile.Profile()
 for _ in range(3):
     t = time.perf_counter()
     pr.enable()
-    plan = pk.run_symbolic(a, p, "allatonce", ctx)
+    plan = pk.run_symbolic(a, p, ALG, ctx)
     torch.cuda.synchronize()
     pr.disable()
     print("wall ms", (time.perf_counter() - t) * 1e3)
