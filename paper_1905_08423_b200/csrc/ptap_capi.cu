@@ -115,6 +115,7 @@ struct ptap_plan {
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool pmap_ready = false;          // position maps written by the row-union pass
   bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
+  double avg_p_row = 4.0;           // P entries per local fine row (arena sizing)
   bool want_maps = false;
   MapArgs maps{};
   MapOut mo{};           // symbolic map outputs (smap, nap) + transient sorted patterns
@@ -513,8 +514,11 @@ ptap_status ap_sizes(ptap_plan *p, const Ops &op, int64_t **ap_nnz_out, cudaStre
 }
 
 unsigned long long local_arena_estimate(const ptap_plan *p, int64_t extra) {
+  // a C row unions the AP rows of its contributors; the wider P's rows, the
+  // more the union outgrows one AP row (27-pt/trilinear: ~1.8x, smoothed
+  // aggregation: ~6x), so scale the average AP row by 1 + (P entries/row)/2
   double avg = p->nloc > 0 ? (double)p->sum_ap / (double)p->nloc : 1.0;
-  double est = (double)p->ncl * (avg * 4.0 + 8.0) + (double)extra;
+  double est = (double)p->ncl * (avg * (1.0 + 0.5 * p->avg_p_row) + 8.0) + (double)extra;
   double bound = (double)p->bound_local + (double)extra;
   if (est > bound) est = bound;
   if (est < 64) est = 64;
@@ -664,10 +668,49 @@ ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
   return PTAP_OK;
 }
 
-// C's structure without an arena (all-at-once, one rank): maps-only outer
-// pass over the local rows, P_d^T, then per C row the union of its
-// contributors' sorted AP rows (k_c_union).  PTAP_ERR_VALUE: some union did
-// not fit the per-row table (the caller then takes the arena path).
+// C rows as unions of pattern rows (CSR pat_rp/pat: AP rows, or the two-step
+// C~ rows) over each C row's contributors (t_rp/t_row: P_d^T).  With pm_op,
+// the fill pass also writes the all-at-once position maps.  PTAP_ERR_VALUE:
+// some union outgrew the per-row table (the caller takes the arena path).
+ptap_status c_rows_by_union(ptap_plan *p, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
+                            const int32_t *pat, const Ops *pm_op, const ptap_operands *pm_ops, cudaStream_t st) {
+  const int64_t ncl = p->ncl;
+  int64_t *cnt = nullptr, *scratch = nullptr;
+  CKS(palloc(p, &cnt, ncl, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(ncl), CAT_TRANSIENT, st));
+  CK(launch_c_union(false, ncl, t_rp, t_row, pat_rp, pat, nullptr, cnt, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, p->d_status, st));
+  int s1 = 0;
+  CKS(read_status(p, st, &s1));
+  ptap_status ret = PTAP_OK;
+  if (s1 & ST_TABLE_FULL) {
+    ret = PTAP_ERR_VALUE;
+  } else {
+    CKS(palloc(p, &p->c_rp, ncl + 1, CAT_OUTPUT, st));
+    CK(scan_exclusive(cnt, p->c_rp, ncl, scratch, st));
+    int64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, p->c_rp + ncl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    p->c_nnz = nnz;
+    CKS(palloc(p, &p->c_col, nnz, CAT_OUTPUT, st));
+    bool pm_ok = false;
+    if (pm_op) CKS(alloc_pmap(p, *pm_op, pm_ops, st, &pm_ok));
+    CK(launch_c_union(true, ncl, t_rp, t_row, pat_rp, pat, nullptr, nullptr, p->c_rp, p->c_col,
+                      pm_ok ? pm_op->pd_rp : nullptr, pm_ok ? pm_op->pd_col : nullptr,
+                      pm_ok ? p->maps.pmap_rp : nullptr, pm_ok ? p->maps.pmap : nullptr, p->d_status, st));
+    p->pmap_ready = pm_ok;
+    p->cnt.kernel_launches += 1;
+  }
+  p->cnt.kernel_launches += 2;
+  pfree(p, cnt, st);
+  pfree(p, scratch, st);
+  return ret;
+}
+
+// C's structure without an arena (all-at-once, a rank that neither sends nor
+// receives): maps-only outer pass over the local rows, P_d^T, then the row
+// unions of the contributors' sorted AP rows, which also write the position
+// maps.
 ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st, Tracer *tr) {
   Arena none{nullptr, 0};
   CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
@@ -693,35 +736,12 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
   CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ncl > 0 ? ncl : 1), st));
   CKS(palloc(p, &t_row, pnnz, CAT_TRANSIENT, st));
   CK(launch_transpose_scatter(p->nloc, op.pd_rp, op.pd_col, t_rp, cnt, t_row, nullptr, st));
-  tr->mark(st, "P_d^T");
-  // row sizes, then the rows
-  CK(launch_c_union(false, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, cnt, nullptr, nullptr, nullptr,
-                    nullptr, nullptr, nullptr, p->d_status, st));
-  int s1 = 0;
-  CKS(read_status(p, st, &s1));
-  ptap_status ret = PTAP_OK;
-  if (s1 & ST_TABLE_FULL) {
-    ret = PTAP_ERR_VALUE;
-  } else {
-    CKS(palloc(p, &p->c_rp, ncl + 1, CAT_OUTPUT, st));
-    CK(scan_exclusive(cnt, p->c_rp, ncl, scratch, st));
-    int64_t nnz = 0;
-    CK(cudaMemcpyAsync(&nnz, p->c_rp + ncl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    p->c_nnz = nnz;
-    CKS(palloc(p, &p->c_col, nnz, CAT_OUTPUT, st));
-    bool pm_ok = false;
-    CKS(alloc_pmap(p, op, ops, st, &pm_ok));
-    CK(launch_c_union(true, ncl, t_rp, t_row, p->mo.pat_rp, p->mo.pat, p->mo.nap, nullptr, p->c_rp, p->c_col,
-                      op.pd_rp, op.pd_col, pm_ok ? p->maps.pmap_rp : nullptr, pm_ok ? p->maps.pmap : nullptr,
-                      p->d_status, st));
-    p->pmap_ready = pm_ok;
-    p->cnt.kernel_launches += 2;
-  }
-  p->cnt.kernel_launches += 4;
+  p->cnt.kernel_launches += 3;
   pfree(p, cnt, st);
-  pfree(p, t_rp, st);
   pfree(p, scratch, st);
+  tr->mark(st, "P_d^T");
+  ptap_status ret = c_rows_by_union(p, t_rp, t_row, p->mo.pat_rp, p->mo.pat, &op, ops, st);
+  pfree(p, t_rp, st);
   pfree(p, t_row, st);
   tr->mark(st, "C rows by unions");
   return ret;
@@ -805,6 +825,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
   Tracer tr;
+  if (p->nloc > 0) p->avg_p_row = (double)(ops->p_diag.nnz + ops->p_off.nnz) / (double)p->nloc;
   CKS(ap_sizes(p, op, &p->ap_nnz, st, &p->apub));
   tr.mark(st, "ap_sizes");
   if (p->alg != PTAP_TWO_STEP) CKS(prepare_maps(p, op, ops, st));
@@ -933,6 +954,13 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
     ptap_status us = c_by_unions(p, op, ops, st, &tr);
     if (us == PTAP_OK) goto c_allocated;
     if (us != PTAP_ERR_VALUE) return us;  // PTAP_ERR_VALUE: a union outgrew the table -> arena path
+  }
+  if (p->alg == PTAP_TWO_STEP && !(recv && recv->nrows > 0) && ops->p_off.nnz == 0 && !getenv("PTAP_NO_UNION")) {
+    // C = P_d^T C~ row by row: unions of the C~ rows of each C row's contributors
+    ptap_status us = c_rows_by_union(p, p->ptd.rp, p->ptd.row, p->ct_rp, p->ct_col, nullptr, nullptr, st);
+    tr.mark(st, "C rows by unions");
+    if (us == PTAP_OK) goto c_allocated;
+    if (us != PTAP_ERR_VALUE) return us;
   }
   if (p->alg != PTAP_MERGED || p->merged_deferred)
     CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st, (unsigned long long)p->ncl));

@@ -238,14 +238,26 @@ cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *ap
 __device__ __forceinline__ void arena_insert(const Arena &a, unsigned long long row, unsigned long long col,
                                              int *status) {
   const unsigned long long key = row * a.m + col;
-  unsigned long long h;
-  if (a.log2b > 0) {
-    const unsigned long long bm = (1ull << a.log2b) - 1ull;
-    h = ((row << a.log2b) | ((unsigned long long)hash32((uint32_t)col, a.log2b) & bm)) & a.mask;
-  } else {
-    h = hash64(key) & a.mask;
-  }
   unsigned long long *ar = a.keys;
+  if (a.log2b > 0) {
+    // inside the row's own run first (wrapping within it); a row longer than
+    // its run continues at a hashed position, so overflow never cascades
+    // into the neighbouring rows' runs
+    const unsigned long long bm = (1ull << a.log2b) - 1ull;
+    const unsigned long long b0 = (row << a.log2b) & a.mask;
+    unsigned long long o = (unsigned long long)hash32((uint32_t)col, a.log2b) & bm;
+    for (unsigned long long probe = 0; probe <= bm; ++probe) {
+      const unsigned long long hh = b0 | o;
+      const unsigned long long k = ar[hh];
+      if (k == key) return;
+      if (k == EMPTY64) {
+        const unsigned long long old = atomicCAS(ar + hh, EMPTY64, key);
+        if (old == EMPTY64 || old == key) return;
+      }
+      o = (o + 1) & bm;
+    }
+  }
+  unsigned long long h = hash64(key) & a.mask;
   for (int probe = 0; probe < 8192; ++probe) {
     unsigned long long k = ar[h];
     if (k == key) return;
@@ -1129,7 +1141,7 @@ cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigne
 // entry (SURVEY §8(a) a6/a7 restated row-wise).  FILL = false counts (and
 // flags rows whose union does not fit the table), FILL = true writes the
 // sorted columns.
-constexpr int CU_LOG2T = 8, CU_T = 1 << CU_LOG2T, CU_MAX = 192;
+constexpr int CU_LOG2T = 9, CU_T = 1 << CU_LOG2T, CU_MAX = 384;
 
 // the contributors' AP entries of C row J, flattened over the warp's lanes
 // 32 contributors at a time; f(g, c_base_pm, s) is called for every entry
@@ -1145,8 +1157,8 @@ __device__ __forceinline__ void cu_sweep(int64_t J, const int64_t *t_rp, const i
     int64_t my_base = 0, my_pm = -1;
     if (lane < nc) {
       const int32_t i = t_row[tb + lane];
-      my_n = nap[i];
       my_base = pat_rp[i];
+      my_n = (int)(pat_rp[i + 1] - my_base);  // pattern rows are a CSR (AP rows or C~ rows)
       if (pmap_rp) {  // where row i's positions for target J go: jj-th block of its map
         const int64_t e0 = pd_rp[i], e1 = pd_rp[i + 1];
         int64_t jj = 0;
@@ -1195,11 +1207,12 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
                                                  const int64_t *pmap_rp, uint8_t *pmap, int *status) {
   __shared__ int32_t keys_all[8][CU_T];
   __shared__ int32_t lk_all[8][CU_T];
-  __shared__ uint8_t lpos_all[8][CU_T];
+  __shared__ uint16_t lpos_all[8][CU_T];
   __shared__ uint8_t rank_all[8][CU_T];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   int32_t *keys = keys_all[warp], *lk = lk_all[warp];
-  uint8_t *lpos = lpos_all[warp], *srank = rank_all[warp];
+  uint16_t *lpos = lpos_all[warp];
+  uint8_t *srank = rank_all[warp];
   for (int64_t J = (int64_t)blockIdx.x * 8 + warp; J < ncl; J += (int64_t)gridDim.x * 8) {
     for (int x = lane; x < CU_T; x += 32) keys[x] = EMPTY32;
     __syncwarp();
@@ -1227,7 +1240,7 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
       if (k != EMPTY32) {
         const int at = n + __popc(b & ((1u << lane) - 1u));
         lk[at] = k;
-        lpos[at] = (uint8_t)(s0 + lane);
+        lpos[at] = (uint16_t)(s0 + lane);
       }
       n += __popc(b);
     }
