@@ -198,3 +198,20 @@ def test_streamed_host_numeric_matches_one_shot():
             del os.environ["PTAP_UPLOAD_BLOCKS"]
         assert row_scaled_err(ip, got, ref) <= 1e-15
     assert plan.counters.numeric_runs == 4
+
+
+def test_streamed_path_falls_back_when_rows_not_range_addressable():
+    """Config-4 rows (wide P rows: > 128 fold pairs) take the generic mapped
+    kernel, so the streamed host pass is declined on the first call and the
+    one-shot path produces C (same values both calls)."""
+    from paper_1905_08423_b200 import problems_amg as amg
+    A, P = amg.block_transport(6)
+    ctx = pk.single_rank_context()
+    a, p = pk.distribute(A, P, 1, 0)
+    plan = pk.run_symbolic(a, p, "allatonce", ctx)
+    c1 = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
+    assert getattr(plan, "_stream_ok", True) is False
+    c2 = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
+    ip = plan.c_alloc.local.diag.row_offsets
+    assert row_scaled_err(ip, c2, c1) <= 1e-15
+    assert plan.counters.numeric_runs == 2
