@@ -86,23 +86,14 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_PF
 #define PTAP_PF 1
 #endif
-#ifndef PTAP_OUTER_SERIAL
-#define PTAP_OUTER_SERIAL 0
-#endif
-#ifndef PTAP_GPAD
-#define PTAP_GPAD 0
-#endif
-#ifndef PTAP_AOFF
-#define PTAP_AOFF 0
-#endif
-// per-group shared region: accumulator (NAPCAP + 1 slots, optionally shifted
-// by PTAP_AOFF bytes), then G step entries and G P_o row starts; PTAP_GPAD
-// pads the region to move successive groups to other shared-memory banks
+// per-group shared region: accumulator (NAPCAP + 1 slots), then G step
+// entries and G P_o row starts (group stride 352 B for <4,32>: successive
+// groups start 12 bank pairs apart -- the best of the strides measured)
 __host__ __device__ constexpr size_t acc_region_bytes(int napcap) {
-  return (((size_t)(napcap + 1) * 8 + PTAP_AOFF + 15) & ~(size_t)15);
+  return (((size_t)(napcap + 1) * 8 + 15) & ~(size_t)15);
 }
 __host__ __device__ constexpr size_t group_bytes(int g, int napcap) {
-  return ((acc_region_bytes(napcap) + (size_t)g * 16 + (size_t)g * 4 + 15) & ~(size_t)15) + PTAP_GPAD;
+  return (acc_region_bytes(napcap) + (size_t)g * 16 + (size_t)g * 4 + 15) & ~(size_t)15;
 }
 
 // Outer-product phase shared by the mapped kernels: the target rows of
@@ -118,34 +109,6 @@ __device__ __forceinline__ void outer_scatter(const Ops &op, const MapArgs &mp, 
   const int nP = ndP + (int)(po1 - po0);
   const int maxj = __reduce_max_sync(FULL, i >= 0 ? nP : 0);
   const int64_t pbase = i >= 0 ? __ldg(mp.pmap_rp + i) : 0;
-#if PTAP_OUTER_SERIAL
-  for (int jj = 0; jj < maxj; ++jj) {
-    bool live = i >= 0 && jj < nP && (jj < ndP ? wl : ws);
-    if (live) {
-      double pij;
-      int64_t base;
-      double *cval;
-      if (jj < ndP) {
-        int32_t J = __ldg(op.pd_col + pd0 + jj);
-        pij = __ldg(op.pd_val + pd0 + jj);
-        base = __ldg(tg.c_rp + J);
-        cval = tg.c_val;
-      } else {
-        int64_t e = po0 + (jj - ndP);
-        pij = __ldg(op.po_val + e);
-        base = __ldg(tg.s_rp + __ldg(mp.po_srow + e));
-        cval = tg.s_val;
-      }
-      const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
-#pragma unroll
-      for (int k = 0; k < NREG; ++k) {
-        int s = gl + G * k;
-        if (s < nap) atomicAdd(cval + base + __ldg(pm + s), __dmul_rn(pij, accr[k]));
-      }
-    }
-  }
-  return;
-#endif
   for (int jb = 0; jb < maxj; jb += G) {
     const int jm = jb + gl;
     double pij = 0.0;
@@ -193,7 +156,7 @@ __global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_m
   // per group: acc[NAPCAP + 1] (f64, +1 pad spreads groups over banks), ent[G], o0[G]
   constexpr size_t gbytes = group_bytes(G, NAPCAP);
   unsigned char *gbase = smem + (size_t)gid * gbytes;
-  double *acc = (double *)(gbase + PTAP_AOFF);
+  double *acc = (double *)gbase;
   StepEntry *ent = (StepEntry *)(gbase + acc_region_bytes(NAPCAP));
   int32_t *ent_o0 = (int32_t *)(ent + G);
   const bool has_po = op.po_rp != nullptr;
