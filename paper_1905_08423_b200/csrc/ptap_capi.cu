@@ -114,6 +114,7 @@ struct ptap_plan {
   bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool pmap_ready = false;          // position maps written by the row-union pass
+  bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
   bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
   double avg_p_row = 4.0;           // P entries per local fine row (arena sizing)
   bool want_maps = false;
@@ -569,6 +570,15 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
                                       ops->p_remote.nnz});
     p->q4 = h[1] <= 128 && p->nloc < lim && nnz_max < lim && !getenv("PTAP_NO_Q4");
     p->q4_sym = p->q4 && !getenv("PTAP_NO_Q4_SYMBOLIC");
+    // q4a (A staged by cp.async): one-rank structure, A rows <= 32 entries
+    if (p->q4 && ops->a_off.nnz == 0 && ops->p_off.nnz == 0 && !getenv("PTAP_NO_Q4A")) {
+      CK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
+      CK(launch_max_rowlen(p->nloc, op.ad_rp, mx, st));
+      unsigned long long amax = 0;
+      CK(cudaMemcpyAsync(&amax, mx, sizeof(amax), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      p->q4a = amax <= 32;
+    }
   }
   int64_t *slen = nullptr, *scratch = nullptr;
   CKS(palloc(p, &slen, p->nloc, CAT_TRANSIENT, st));
@@ -753,6 +763,11 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
     for (int q = 0; q < NBINS; ++q) {
       if (bs.count[q] == 0) continue;
       const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
+      if (q == 0 && p->q4a && bs.identity0 && do_local && !do_send) {
+        CK(launch_outer_numeric_q4a(op, (unsigned long long)bs.count[q], p->maps, tg, p->d_status, st, 0));
+        p->cnt.kernel_launches++;
+        continue;
+      }
       CK(launch_outer_numeric_mapped(q == 0 ? (p->q4 ? 3 : 0) : 1, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
                                      do_local, p->d_status, st));
       p->cnt.kernel_launches++;
@@ -1106,8 +1121,12 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
   if ((flags & 1) && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   if (row_hi > row_lo) {
-    CK(launch_outer_numeric_mapped(3, op, nullptr, (unsigned long long)(row_hi - row_lo), p->maps, tg, 0, 1,
-                                   p->d_status, st, (int)row_lo));
+    if (p->q4a)
+      CK(launch_outer_numeric_q4a(op, (unsigned long long)(row_hi - row_lo), p->maps, tg, p->d_status, st,
+                                  (int)row_lo));
+    else
+      CK(launch_outer_numeric_mapped(3, op, nullptr, (unsigned long long)(row_hi - row_lo), p->maps, tg, 0, 1,
+                                     p->d_status, st, (int)row_lo));
     p->cnt.kernel_launches++;
     p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
   }

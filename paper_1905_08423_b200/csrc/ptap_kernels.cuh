@@ -152,6 +152,8 @@ cudaError_t launch_max_rowlen(int64_t n, const int64_t *rp, unsigned long long *
 cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                         const MapArgs &mp, const OuterTargets &tg, int do_send, int do_local,
                                         int *status, cudaStream_t st, int row0 = 0);
+cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, const MapArgs &mp,
+                                     const OuterTargets &tg, int *status, cudaStream_t st, int row0 = 0);
 cudaError_t launch_c_last_row(int64_t n, const int64_t *pd_rp, const int32_t *pd_col, int64_t ncl, int32_t *last,
                               cudaStream_t st);
 
