@@ -538,8 +538,9 @@ __device__ __forceinline__ void qa_stage(const Ops &op, const MapArgs &mp, Q4War
                                          int lane) {
   const int r1 = min(r0 + Q4_RPW, total);
   const int a0 = (int)__ldg(op.ad_rp + r0), a1 = (int)__ldg(op.ad_rp + r1);
+  const int32_t *csrc = mp.poff ? mp.poff : op.ad_col;  // packed P row bounds, or A's columns
   for (int q = lane; q < a1 - a0; q += 32) {
-    cp_async4(&S.col[q], op.ad_col + a0 + q);
+    cp_async4(&S.col[q], csrc + a0 + q);
 #if PTAP_QA_VALS
     cp_async8(&S.val[q], op.ad_val + a0 + q);
 #endif
@@ -597,8 +598,13 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
 #else
         a = __ldg(op.ad_val + a0 + t0 + t);
 #endif
-        d0 = (int)__ldg(op.pd_rp + k);
-        plen = (int)__ldg(op.pd_rp + k + 1) - d0;
+        if (mp.poff) {
+          d0 = k & 0x0fffffff;
+          plen = (int)((unsigned)k >> 28);
+        } else {
+          d0 = (int)__ldg(op.pd_rp + k);
+          plen = (int)__ldg(op.pd_rp + k + 1) - d0;
+        }
       }
       int incl = plen;
 #pragma unroll
@@ -672,6 +678,23 @@ cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, co
   unsigned long long grid = (nrows + rpc - 1) / rpc;
   grid = std::min(grid, grid_cap(k_outer_numeric_q4a, warps * 32, sm));
   k_outer_numeric_q4a<<<(int)grid, warps * 32, sm, st>>>(op, nrows, mp, tg, status, row0);
+  return cudaGetLastError();
+}
+
+// poff[e] = P_rp[k] | (P_rp[k+1] - P_rp[k]) << 28 for A entry e with column k
+// (the plan checks nnz(P_d) < 2^28 and P rows <= 15): the q4a fold reads this
+// instead of A's column and P's row bounds, one dependent load less per chunk
+__global__ void k_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const int32_t k = ad_col[e];
+  const int64_t x0 = pd_rp[k];
+  poff[e] = (int32_t)(x0 | ((pd_rp[k + 1] - x0) << 28));
+}
+
+cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,
+                              cudaStream_t st) {
+  if (nnz > 0) k_build_poff<<<nb(nnz, 256), 256, 0, st>>>(nnz, ad_col, pd_rp, poff);
   return cudaGetLastError();
 }
 
