@@ -1075,6 +1075,7 @@ static ptap_status numeric_ready(ptap_plan *p) {
 
 ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stream) {
   CKS(numeric_ready(p));
+  CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
   if (p->alg == PTAP_TWO_STEP) {
@@ -1102,6 +1103,7 @@ ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stre
 
 ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *stream) {
   CKS(numeric_ready(p));
+  CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
   if (p->alg == PTAP_TWO_STEP) {
@@ -1123,6 +1125,7 @@ ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *str
 ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int64_t row_lo, int64_t row_hi,
                                     int flags, void *stream) {
   CKS(numeric_ready(p));
+  CKS(validate(ops));
   if (p->alg != PTAP_ALLATONCE || !p->mapped || !p->q4 || !p->bins_local.identity0)
     return fail(PTAP_ERR_VALUE, "plan has no range-addressable local rows");
   if (row_lo < 0 || row_hi > p->nloc || row_lo > row_hi) return fail(PTAP_ERR_VALUE, "row range");
@@ -1146,6 +1149,8 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
 
 ptap_status ptap_plan_c_last_row(ptap_plan *p, const ptap_operands *ops, int32_t *last, void *stream) {
   CKS(numeric_ready(p));
+  CKS(validate(ops));
+  if (!last && p->ncl > 0) return fail(PTAP_ERR_VALUE, "null output");
   CK(launch_c_last_row(p->nloc, ops->p_diag.row_ptr, ops->p_diag.col, p->ncl, last, (cudaStream_t)stream));
   return PTAP_OK;
 }

@@ -49,3 +49,23 @@ def test_status_codes_map_to_reference_exceptions():
     assert _lib._STATUS_EXC[3] is StructuralDriftError
     assert _lib._STATUS_EXC[4] is OwnershipError
     assert _lib._STATUS_EXC[5] is DeviceError
+
+
+def test_null_and_bad_arguments_are_status_codes():
+    """Host-side validation of every phase entry point: null plan/operands or
+    an unknown algorithm come back as PTAP_ERR_VALUE (1) with a message, never
+    as a crash (no device needed: nothing reaches a kernel)."""
+    import ctypes
+    L = _lib.load(require_device=False)
+    null = ctypes.c_void_p(0)
+    out = ctypes.c_void_p()
+    assert L.ptap_plan_create(7, None, ctypes.byref(out)) == 1
+    assert b"algorithm" in L.ptap_last_error()
+    assert L.ptap_plan_create(1, None, ctypes.byref(out)) == 1
+    for fn in ("ptap_symbolic_send", "ptap_numeric_send", "ptap_numeric_local"):
+        assert getattr(L, fn)(null, None, null) == 1, fn
+    assert L.ptap_symbolic_local(null, None, None, null) == 1
+    assert L.ptap_numeric_local_rows(null, None, 0, 0, 0, null) == 1
+    assert L.ptap_plan_c_last_row(null, None, null, null) == 1
+    assert L.ptap_plan_check(null, null) == 1
+    assert b"null plan" in L.ptap_last_error()
