@@ -100,3 +100,20 @@ def test_golden_parity_many_ranks(case, nr):
             assert np.array_equal(c.values.view(np.uint64), v.view(np.uint64)), (alg, "bit-exact")
         else:
             assert row_scaled_err(ip, c.values, v) <= TOL, alg
+
+
+def test_config2_full_size_against_oracle():
+    """BASELINE config 2 at its full size (7-point Poisson 128^3 -> 64^3,
+    2.1 M rows): every algorithm on the GPU against the CPU oracle.  The
+    inputs are dyadic, so all three must be bit-exact."""
+    from oracle.oracle import oracle_ptap
+    from paper_1905_08423_b200 import problems as gen
+    A, P = gen.config_operands(gen.CONFIGS["cfg2"])
+    assert A.nrows == 128 ** 3 and P.ncols == 64 ** 3
+    want = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values,
+                       P.row_offsets, P.col_indices, P.values, nranks=1, algorithm="allatonce")
+    for alg in ("two-step", "allatonce", "merged"):
+        c, _ = run_ptap(A, P, 1, alg)
+        assert np.array_equal(c.row_offsets, want.row_ptr), alg
+        assert np.array_equal(c.col_indices, want.col), alg
+        assert np.array_equal(c.values.view(np.uint64), want.val.view(np.uint64)), alg
