@@ -667,6 +667,12 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     }
   }
   p->mapped = ok;
+  // C row start per P_d entry for the q4a outer phase (4 B per P entry)
+  if (ok && p->q4a && p->c_nnz < INT32_MAX && !getenv("PTAP_NO_CBASE")) {
+    CKS(palloc(p, &p->maps.cbase, ops->p_diag.nnz, CAT_PLAN, st));
+    CK(launch_build_cbase(ops->p_diag.nnz, op.pd_col, p->c_rp, p->maps.cbase, st));
+    p->cnt.kernel_launches++;
+  }
   pfree(p, p->pat, st);
   pfree(p, p->pat_rp, st);
   p->mo = MapOut{};
@@ -683,7 +689,7 @@ ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
   pfree(p, p->maps.smap_rp, st); pfree(p, p->maps.pmap_rp, st);
   pfree(p, p->maps.smap, st); pfree(p, p->maps.pmap, st);
   pfree(p, p->maps.nap, st); pfree(p, p->maps.po_srow, st);
-  pfree(p, p->maps.poff, st);
+  pfree(p, p->maps.poff, st); pfree(p, p->maps.cbase, st);
   p->mapped = false;
   return PTAP_OK;
 }

@@ -58,6 +58,7 @@ struct MapArgs {
   uint8_t *nap;      // [nloc] AP row sizes
   int32_t *po_srow;  // [nnz(P_o)] staging row of every P_o entry
   int32_t *poff;     // [nnz(A_d)] q4a: start of the entry's P row | (its length << 28); null: unused
+  int32_t *cbase;    // [nnz(P_d)] q4a: start of the C row each P_d entry targets; null: unused
 };
 
 struct LaunchShape {
@@ -157,6 +158,8 @@ cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, co
                                      const OuterTargets &tg, int *status, cudaStream_t st, int row0 = 0);
 cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,
                               cudaStream_t st);
+cudaError_t launch_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t *c_rp, int32_t *cbase,
+                               cudaStream_t st);
 cudaError_t launch_c_last_row(int64_t n, const int64_t *pd_rp, const int32_t *pd_col, int64_t ncl, int32_t *last,
                               cudaStream_t st);
 

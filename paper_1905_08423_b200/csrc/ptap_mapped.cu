@@ -501,6 +501,39 @@ static unsigned long long resident(K kern, int threads, size_t smem) {
 
 static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 
+// q4a outer phase with the C-row-start map: every lane of a row's group reads
+// each target's (C row start, P value) directly (one broadcast load each, two
+// targets in flight), no shuffles, no column -> row-pointer chain
+template <int G, int NREG>
+__device__ __forceinline__ void outer_scatter_cb(const Ops &op, const MapArgs &mp, const OuterTargets &tg, int i,
+                                                 int pd0, int pd1, int nap, const double (&accr)[NREG], int gl) {
+  const int nP = i >= 0 ? pd1 - pd0 : 0;
+  const int maxj = __reduce_max_sync(FULL, nP);
+  const int64_t pbase = i >= 0 ? __ldg(mp.pmap_rp + i) : 0;
+  for (int jj = 0; jj < maxj; jj += 2) {
+    int b0 = -1, b1 = -1;
+    double v0 = 0.0, v1 = 0.0;
+    if (jj < nP) { b0 = __ldg(mp.cbase + pd0 + jj); v0 = __ldg(op.pd_val + pd0 + jj); }
+    if (jj + 1 < nP) { b1 = __ldg(mp.cbase + pd0 + jj + 1); v1 = __ldg(op.pd_val + pd0 + jj + 1); }
+    if (b0 >= 0) {
+      const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
+#pragma unroll
+      for (int k = 0; k < NREG; ++k) {
+        const int s = gl + G * k;
+        if (s < nap) atomicAdd(tg.c_val + b0 + __ldg(pm + s), __dmul_rn(v0, accr[k]));
+      }
+    }
+    if (b1 >= 0) {
+      const uint8_t *pm = mp.pmap + pbase + (int64_t)(jj + 1) * nap;
+#pragma unroll
+      for (int k = 0; k < NREG; ++k) {
+        const int s = gl + G * k;
+        if (s < nap) atomicAdd(tg.c_val + b1 + __ldg(pm + s), __dmul_rn(v1, accr[k]));
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // q4a: the bin-0 kernel for one-rank structure (identity rows, no A_o/P_o,
 // A rows <= 32 entries) with the next batch's A columns and slot maps copied
@@ -662,7 +695,10 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
     double accr[NREG];
 #pragma unroll
     for (int q = 0; q < NREG; ++q) accr[q] = (gl + G * q < nap) ? acc[gl + G * q] : 0.0;
-    outer_scatter<G, NREG>(op, mp, tg, i, pd0, pd1, 0, 0, wl, false, nap, accr, gl);
+    if (mp.cbase)
+      outer_scatter_cb<G, NREG>(op, mp, tg, i, pd0, pd1, nap, accr, gl);
+    else
+      outer_scatter<G, NREG>(op, mp, tg, i, pd0, pd1, 0, 0, wl, false, nap, accr, gl);
   }
   cp_async_wait_all();
 }
@@ -695,6 +731,19 @@ __global__ void k_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *
 cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,
                               cudaStream_t st) {
   if (nnz > 0) k_build_poff<<<nb(nnz, 256), 256, 0, st>>>(nnz, ad_col, pd_rp, poff);
+  return cudaGetLastError();
+}
+
+// cbase[e] = C row start of the row P_d entry e targets (the outer phase of
+// q4a reads it instead of the column -> C row pointer chain)
+__global__ void k_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t *c_rp, int32_t *cbase) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) cbase[e] = (int32_t)c_rp[pd_col[e]];
+}
+
+cudaError_t launch_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t *c_rp, int32_t *cbase,
+                               cudaStream_t st) {
+  if (nnz > 0) k_build_cbase<<<nb(nnz, 256), 256, 0, st>>>(nnz, pd_col, c_rp, cbase);
   return cudaGetLastError();
 }
 
