@@ -114,6 +114,7 @@ struct ptap_plan {
   bool q4 = false;                  // bin 0 runs k_outer_numeric_q4
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool pmap_ready = false;          // position maps written by the row-union pass
+  bool smap_interned = false;       // slot maps already interned (row-union path)
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
   bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
   double avg_p_row = 4.0;           // P entries per local fine row (arena sizing)
@@ -642,12 +643,71 @@ ptap_status alloc_pmap(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   pfree(p, unused, st);
   pfree(p, scratch, st);
   p->pmap_bytes = tot;
-  CKS(palloc(p, &p->maps.pmap, tot, CAT_PLAN, st));
+  CKS(palloc(p, &p->maps.pmap, tot + 16, CAT_PLAN, st));  // padded: interned word-wise
   int64_t po_nnz = ops->p_off.nnz;
   CKS(palloc(p, &p->maps.po_srow, po_nnz, CAT_PLAN, st));
   if (po_nnz > 0)
     CK(launch_po_srow(po_nnz, op.po_col, op.p_colmap, p->s_nrows, p->s_rows, p->maps.po_srow, p->d_status, st));
   p->cnt.kernel_launches += 4;
+  return PTAP_OK;
+}
+
+// Interns a per-row byte map (src at monotone offsets src_rp[0..n]) into a
+// pool holding each distinct row map once (word aligned); src and src_rp are
+// replaced by the pool and the per-row pool offsets (| length << 40 with
+// pack_len).  Three kernels (claim, resolve, copy) around one scan; see
+// k_intern_claim.
+ptap_status intern_map(ptap_plan *p, uint8_t *&src, int64_t *&src_rp, int64_t n, int64_t total, bool pack_len,
+                       int64_t *pool_bytes, cudaStream_t st) {
+  if (getenv("PTAP_NO_INTERN")) {
+    if (pack_len) {  // same packed layout without sharing: offset | length << 40
+      int64_t *out = nullptr;
+      CKS(palloc(p, &out, n + 1, CAT_PLAN, st));
+      CK(launch_pack_offsets(n, src_rp, out, st));
+      p->cnt.kernel_launches++;
+      pfree(p, src_rp, st);
+      src_rp = out;
+    }
+    *pool_bytes = total;
+    return PTAP_OK;
+  }
+  int64_t ent = 1024;
+  while (ent < 2 * n && ent < (int64_t(1) << 22)) ent <<= 1;
+  unsigned long long *keys = nullptr;
+  int64_t *vals = nullptr, *slot_of = nullptr, *owner = nullptr, *words = nullptr, *wpos = nullptr,
+          *scratch = nullptr, *out = nullptr;
+  CKS(palloc(p, &keys, ent, CAT_TRANSIENT, st));
+  CKS(palloc(p, &vals, ent, CAT_TRANSIENT, st));
+  CKS(palloc(p, &slot_of, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &owner, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &words, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &wpos, n + 1, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(n), CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * ent, st));
+  CK(launch_intern(0, n, src, src_rp, keys, vals, (unsigned long long)(ent - 1), slot_of, owner, words, nullptr,
+                   nullptr, 0, st));
+  CK(launch_intern(1, n, src, src_rp, keys, vals, 0, slot_of, owner, words, nullptr, nullptr, 0, st));
+  pfree(p, keys, st);
+  pfree(p, vals, st);
+  pfree(p, slot_of, st);
+  CK(scan_exclusive(words, wpos, n, scratch, st));
+  int64_t nw = 0;
+  CK(cudaMemcpyAsync(&nw, wpos + n, sizeof(nw), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  uint8_t *pool = nullptr;
+  CKS(palloc(p, &pool, nw * 4 + 16, CAT_PLAN, st));  // +16: the numeric kernels stage maps as words
+  CKS(palloc(p, &out, n + 1, CAT_PLAN, st));
+  CK(launch_intern(2, n, src, src_rp, nullptr, nullptr, 0, nullptr, owner, wpos, pool, out, pack_len ? 1 : 0, st));
+  p->cnt.kernel_launches += 4;
+  pfree(p, owner, st);
+  pfree(p, words, st);
+  pfree(p, wpos, st);
+  pfree(p, scratch, st);
+  pfree(p, src, st);
+  pfree(p, src_rp, st);
+  src = pool;
+  src_rp = out;
+  *pool_bytes = nw * 4;
   return PTAP_OK;
 }
 
@@ -676,6 +736,12 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   pfree(p, p->pat, st);
   pfree(p, p->pat_rp, st);
   p->mo = MapOut{};
+  if (ok) {
+    if (!p->smap_interned)
+      CKS(intern_map(p, p->maps.smap, p->maps.smap_rp, p->nloc, p->smap_bytes, true, &p->smap_bytes, st));
+    p->smap_interned = true;
+    CKS(intern_map(p, p->maps.pmap, p->maps.pmap_rp, p->nloc, p->pmap_bytes, false, &p->pmap_bytes, st));
+  }
   if (!ok) {
     pfree(p, p->maps.smap_rp, st);
     pfree(p, p->maps.smap, st);
@@ -749,6 +815,13 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
   CKS(read_status(p, st, &s0));
   CKS(status_to_error(s0, "symbolic"));
   tr->mark(st, "local outer symbolic (maps)");
+  if (p->mo.smap) {  // the slot maps are complete: intern them before C's pass
+    CKS(intern_map(p, p->maps.smap, p->maps.smap_rp, p->nloc, p->smap_bytes, true, &p->smap_bytes, st));
+    p->mo.smap = nullptr;
+    p->mo.smap_rp = nullptr;
+    p->smap_interned = true;
+    tr->mark(st, "slot maps interned");
+  }
   // P_d^T structure: fine rows contributing to each local C row
   const int64_t ncl = p->ncl, pnnz = ops->p_diag.nnz;
   int64_t *cnt = nullptr, *t_rp = nullptr, *scratch = nullptr;

@@ -51,9 +51,9 @@ struct MapOut {  // symbolic outputs of the outer-product pass (null: no maps)
 };
 
 struct MapArgs {
-  int64_t *smap_rp;  // [nloc+1] offsets into smap
+  int64_t *smap_rp;  // [nloc] pool offset | map length << 40 (interned maps)
   uint8_t *smap;     // slot of every (A entry, P entry) pair, fold order
-  int64_t *pmap_rp;  // [nloc+1] offsets into pmap
+  int64_t *pmap_rp;  // [nloc] pool offset of the row's position map (interned)
   uint8_t *pmap;     // position of every slot in every target row of P(i,:)
   uint8_t *nap;      // [nloc] AP row sizes
   int32_t *po_srow;  // [nnz(P_o)] staging row of every P_o entry
@@ -156,6 +156,12 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
                                         int *status, cudaStream_t st, int row0 = 0);
 cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, const MapArgs &mp,
                                      const OuterTargets &tg, int *status, cudaStream_t st, int row0 = 0);
+cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cudaStream_t st);
+cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t *src_rp, unsigned long long *keys,
+                          int64_t *vals, unsigned long long mask, int64_t *slot_of, int64_t *owner, int64_t *words,
+                          uint8_t *pool, int64_t *out, int pack_len, cudaStream_t st);
+// packed smap_rp entries of an interned plan: pool offset | map length << 40
+constexpr unsigned long long SMAP_OFF_MASK = (1ull << 40) - 1;
 cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,
                               cudaStream_t st);
 cudaError_t launch_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t *c_rp, int32_t *cbase,

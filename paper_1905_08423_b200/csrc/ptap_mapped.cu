@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_m
     int nap = i >= 0 ? (int)__ldg(mp.nap + i) : 0;
     if (nap > 127)  // no first-touch flags in the map: zero-fill
       for (int s = gl; s < nap; s += G) acc[s] = 0.0;
-    int64_t sbase = i >= 0 ? __ldg(mp.smap_rp + i) : 0;
+    int64_t sbase = i >= 0 ? (int64_t)(__ldg(mp.smap_rp + i) & SMAP_OFF_MASK) : 0;
     const uint8_t *smap = mp.smap + sbase;
     int run = 0;
     __syncwarp();
@@ -419,27 +419,20 @@ __global__ void __launch_bounds__(256, PTAP_MINB) k_outer_numeric_q4(Ops op, con
   for (int r0 = (blockIdx.x * nwarps + warp) * Q4_RPW; r0 < total; r0 += gridDim.x * nwarps * Q4_RPW) {
     const int ridx = r0 + r;
     int i = ridx < total ? (rows ? rows[ridx] : row0 + ridx) : -1;
-    const int i0 = __shfl_sync(FULL, i, 0);
-    const bool contig = __all_sync(FULL, i >= 0 && i == i0 + r);
     bool wl = false, ws = false;
     if (i >= 0) {
       wl = do_local && __ldg(op.pd_rp + i + 1) > __ldg(op.pd_rp + i);
       ws = do_send && has_po && __ldg(op.po_rp + i + 1) > __ldg(op.po_rp + i);
     }
-    const int sb = i >= 0 ? (int)__ldg(mp.smap_rp + i) : 0;
-    // slot maps -> shared: one coalesced sweep for a consecutive batch, else
-    // row by row (the plan guarantees <= 128 map bytes per row)
+    // slot maps -> shared, row by row (interned maps: <= 128 bytes per row at
+    // its pool offset; 33 words per row cover any 4-byte misalignment)
     int sbo;
     __syncwarp();
-    if (contig) {
-      const int wb0 = __shfl_sync(FULL, sb, 0) >> 2;
-      const int we = ((int)__ldg(mp.smap_rp + i0 + Q4_RPW) + 3) >> 2;
-      const uint32_t *src = (const uint32_t *)mp.smap + wb0;
-      for (int q = lane; q < we - wb0; q += 32) W.sm[q] = __ldg(src + q);
-      sbo = sb - wb0 * 4;
-    } else {
+    {
+      const unsigned long long sx = i >= 0 ? __ldg(mp.smap_rp + i) : 0ull;
+      const int sb = (int)(sx & SMAP_OFF_MASK), slen = (int)(sx >> 40);
       if (i >= 0) {
-        const int wb = sb >> 2, we = ((int)__ldg(mp.smap_rp + i + 1) + 3) >> 2;
+        const int wb = sb >> 2, we = (sb + slen + 3) >> 2;
         const uint32_t *src = (const uint32_t *)mp.smap + wb;
         for (int q = gl; q < we - wb; q += G) W.sm[r * 33 + q] = __ldg(src + q);
       }
@@ -578,9 +571,16 @@ __device__ __forceinline__ void qa_stage(const Ops &op, const MapArgs &mp, Q4War
     cp_async8(&S.val[q], op.ad_val + a0 + q);
 #endif
   }
-  const int wb = (int)(__ldg(mp.smap_rp + r0) >> 2), we = (int)((__ldg(mp.smap_rp + r1) + 3) >> 2);
-  const uint32_t *src = (const uint32_t *)mp.smap + wb;
-  for (int q = lane; q < we - wb; q += 32) cp_async4(&W.sm[q], src + q);
+  // slot maps row by row: rows of one class share an interned map, so a
+  // batch's maps are not one contiguous run
+  const int i = r0 + (lane >> 2);
+  if (i < r1) {
+    const unsigned long long sx = __ldg(mp.smap_rp + i);
+    const int sb = (int)(sx & SMAP_OFF_MASK), slen = (int)(sx >> 40);
+    const int wb = sb >> 2, nw = ((sb + slen + 3) >> 2) - wb;
+    const uint32_t *src = (const uint32_t *)mp.smap + wb;
+    for (int q = lane & 3; q < nw; q += 4) cp_async4(&W.sm[(lane >> 2) * 33 + q], src + q);
+  }
   cp_async_commit();
 }
 
@@ -605,12 +605,11 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
     if (i >= 0) { pd0 = (int)__ldg(op.pd_rp + i); pd1 = (int)__ldg(op.pd_rp + i + 1); }
     const bool wl = pd1 > pd0;
     const int a0 = (int)__ldg(op.ad_rp + r0);
-    const int sw0 = (int)(__ldg(mp.smap_rp + r0) >> 2);
     int t0 = 0, len = 0, sbo = 0;
     if (i >= 0) {
       t0 = (int)__ldg(op.ad_rp + i) - a0;
       len = (int)__ldg(op.ad_rp + i + 1) - a0 - t0;
-      sbo = (int)__ldg(mp.smap_rp + i) - sw0 * 4;
+      sbo = r * 132 + (int)(__ldg(mp.smap_rp + i) & 3);
     }
     if (!wl) i = -1;
     if (i < 0) len = 0;
@@ -714,6 +713,162 @@ cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, co
   unsigned long long grid = (nrows + rpc - 1) / rpc;
   grid = std::min(grid, grid_cap(k_outer_numeric_q4a, warps * 32, sm));
   k_outer_numeric_q4a<<<(int)grid, warps * 32, sm, st>>>(op, nrows, mp, tg, status, row0);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Map interning.  The per-row slot and position maps depend only on the
+// row's structure relative to its own AP row and target rows, so rows of the
+// same structural class (every interior row of a stencil's parity class, every
+// node of an aggregate position in smoothed aggregation) carry byte-identical
+// maps.  k_intern stores each distinct byte string once: a warp hashes its
+// row's string, probes an open-addressed table of (hash -> pool offset); the
+// first warp to claim a hash copies the string into the pool and publishes its
+// offset, later warps with the same hash wait for the publication and compare
+// the bytes (a collision keeps probing).  Rows whose probe sequence runs out
+// get a private copy, so the result is exact whatever the table holds.
+// out[i] = pool offset (| length << 40 when pack_len).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+constexpr int INTERN_PROBES = 64, INTERN_G = 8;
+
+// 32-bit word w of a string of len bytes starting at byte address s (any
+// alignment), zero past the end: pool entries are word aligned, zero padded
+__device__ __forceinline__ uint32_t intern_word(const uint8_t *s, int len, int w) {
+  const uintptr_t a = (uintptr_t)s + 4 * w;
+  const uint32_t *p = (const uint32_t *)(a & ~(uintptr_t)3);
+  const int sh = (int)(a & 3) * 8;
+  uint32_t x = p[0];
+  if (sh) x = __funnelshift_r(x, p[1], sh);
+  const int rem = len - 4 * w;
+  return rem >= 4 ? x : (x & ((1u << (8 * rem)) - 1u));
+}
+
+// Three passes, no waiting between warps: (1) claim: each row hashes its
+// string and finds or claims the table slot of that hash (the claiming row
+// becomes the class representative); (2) resolve: each row compares its bytes
+// with its representative's (both in the source maps) and keeps the
+// representative as owner when equal, itself otherwise (a hash collision or
+// no slot: a private copy); (3) after a scan of the owners' word counts,
+// owners copy their strings into the pool and every row records its owner's
+// pool offset.  INTERN_G lanes per row, 4 rows per warp.
+__device__ __forceinline__ unsigned long long intern_hash(const uint8_t *s, int len, int gl, unsigned gmask) {
+  constexpr int G = INTERN_G;
+  const int nwords = (len + 3) >> 2;
+  unsigned long long h = 0;
+  for (int w = gl; w < nwords; w += G) h += mix64(((unsigned long long)w << 32) | intern_word(s, len, w));
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) h += __shfl_xor_sync(gmask, h, o, G);
+  h = mix64(h ^ ((unsigned long long)len << 40));
+  return h ? h : 1;
+}
+
+__global__ void __launch_bounds__(256) k_intern_claim(int64_t n, const uint8_t *src, const int64_t *src_rp,
+                                                      unsigned long long *keys, int64_t *vals,
+                                                      unsigned long long mask, int64_t *slot_of) {
+  constexpr int G = INTERN_G;
+  const int lane = lane_id(), gl = lane & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += ng) {
+    const int64_t s0 = src_rp[i];
+    const int len = (int)(src_rp[i + 1] - s0);
+    if (len == 0) {
+      if (gl == 0) slot_of[i] = -1;
+      continue;
+    }
+    const unsigned long long h = intern_hash(src + s0, len, gl, gmask);
+    if (gl == 0) {
+      unsigned long long slot = h & mask;
+      int64_t found = -1;
+      for (int probe = 0; probe < INTERN_PROBES; ++probe) {
+        unsigned long long k = keys[slot];  // a stale 0 only costs a CAS
+        if (k == 0) {
+          k = atomicCAS(keys + slot, 0ull, h);
+          if (k == 0) vals[slot] = i;  // the representative; read after this kernel
+        }
+        if (k == 0 || k == h) { found = (int64_t)slot; break; }
+        slot = (slot + 1) & mask;
+      }
+      slot_of[i] = found;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_intern_resolve(int64_t n, const uint8_t *src, const int64_t *src_rp,
+                                                        const int64_t *vals, const int64_t *slot_of,
+                                                        int64_t *owner, int64_t *words) {
+  constexpr int G = INTERN_G;
+  const int lane = lane_id(), gl = lane & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += ng) {
+    const int64_t s0 = __ldg(src_rp + i);
+    const int len = (int)(__ldg(src_rp + i + 1) - s0);
+    const int64_t sl = __ldg(slot_of + i);
+    int64_t own = i;
+    if (len > 0 && sl >= 0) {
+      const int64_t rep = __ldg(vals + sl);
+      if (rep != i) {
+        const int64_t r0 = __ldg(src_rp + rep);
+        bool eq = __ldg(src_rp + rep + 1) - r0 == len;
+        if (eq) {
+          const int nwords = (len + 3) >> 2;
+          for (int w = gl; w < nwords; w += G) eq &= intern_word(src + s0, len, w) == intern_word(src + r0, len, w);
+        }
+        if (__all_sync(gmask, eq)) own = rep;
+      }
+    }
+    if (gl == 0) {
+      owner[i] = own;
+      words[i] = own == i ? (int64_t)((len + 3) >> 2) : 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_intern_copy(int64_t n, const uint8_t *src, const int64_t *src_rp,
+                                                     const int64_t *owner, const int64_t *wpos, uint8_t *pool,
+                                                     int64_t *out, int pack_len) {
+  constexpr int G = INTERN_G;
+  const int lane = lane_id(), gl = lane & (G - 1);
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += ng) {
+    const int64_t s0 = src_rp[i];
+    const int len = (int)(src_rp[i + 1] - s0);
+    const int64_t own = owner[i];
+    const int64_t off = wpos[own] * 4;
+    if (own == i) {
+      uint32_t *pw = (uint32_t *)(pool + off);
+      for (int w = gl; w < ((len + 3) >> 2); w += G) pw[w] = intern_word(src + s0, len, w);
+    }
+    if (gl == 0) out[i] = pack_len ? (off | ((int64_t)len << 40)) : off;
+  }
+}
+
+__global__ void k_pack_offsets(int64_t n, const int64_t *rp, int64_t *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = rp[i] | ((rp[i + 1] - rp[i]) << 40);
+}
+
+cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cudaStream_t st) {
+  if (n > 0) k_pack_offsets<<<nb(n, 256), 256, 0, st>>>(n, rp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t *src_rp, unsigned long long *keys,
+                          int64_t *vals, unsigned long long mask, int64_t *slot_of, int64_t *owner, int64_t *words,
+                          uint8_t *pool, int64_t *out, int pack_len, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 31) / 32, 148 * 32);
+  if (pass == 0) k_intern_claim<<<blocks, 256, 0, st>>>(n, src, src_rp, keys, vals, mask, slot_of);
+  else if (pass == 1) k_intern_resolve<<<blocks, 256, 0, st>>>(n, src, src_rp, vals, slot_of, owner, words);
+  else k_intern_copy<<<blocks, 256, 0, st>>>(n, src, src_rp, owner, words, pool, out, pack_len);
   return cudaGetLastError();
 }
 

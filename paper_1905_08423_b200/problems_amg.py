@@ -134,7 +134,7 @@ def block_transport(nn: int, ncomp: int = 10, seed: int = 20190520, agg: int = 3
     return _to_csr(A), _to_csr(P)
 
 
-def _greedy_aggregate(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.ndarray:
+def _greedy_aggregate_py(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.ndarray:
     """Greedy distance-2 aggregation in natural order (see module docstring)."""
     agg = np.full(n, -1, np.int64)
     nagg = 0
@@ -158,6 +158,58 @@ def _greedy_aggregate(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.nda
     return agg
 
 
+def _greedy_aggregate_loops(indptr, indices, n):
+    """The same two passes as _greedy_aggregate_py, as scalar loops (numba)."""
+    agg = np.full(n, -1, np.int64)
+    nagg = 0
+    for i in range(n):
+        if agg[i] >= 0:
+            continue
+        free = True
+        for q in range(indptr[i], indptr[i + 1]):
+            j = indices[q]
+            if j != i and agg[j] >= 0:
+                free = False
+                break
+        if free:
+            agg[i] = nagg
+            for q in range(indptr[i], indptr[i + 1]):
+                agg[indices[q]] = nagg
+            nagg += 1
+    # second pass: a leftover joins the aggregate of its smallest-index
+    # aggregated neighbour (leftovers assigned earlier in this pass count)
+    for i in range(n):
+        if agg[i] >= 0:
+            continue
+        best = -1
+        for q in range(indptr[i], indptr[i + 1]):
+            j = indices[q]
+            if j != i and agg[j] >= 0 and (best < 0 or j < best):
+                best = j
+        if best >= 0:
+            agg[i] = agg[best]
+        else:
+            agg[i] = nagg
+            nagg += 1
+    return agg
+
+
+def _greedy_aggregate(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.ndarray:
+    """Greedy distance-2 aggregation (numba-compiled loops when numba is
+    importable, else the numpy version; both give the same aggregates)."""
+    try:
+        import numba
+    except ImportError:
+        return _greedy_aggregate_py(indptr, indices, n)
+    global _greedy_jit
+    if _greedy_jit is None:
+        _greedy_jit = numba.njit(cache=False)(_greedy_aggregate_loops)
+    return _greedy_jit(indptr.astype(np.int64), indices.astype(np.int64), n)
+
+
+_greedy_jit = None
+
+
 def knn_laplacian(npts: int, k: int = 26, seed: int = 20190520):
     """Config 5 at npts points: returns (A, P) as CsrMatrix."""
     import scipy.sparse as sp
@@ -165,18 +217,16 @@ def knn_laplacian(npts: int, k: int = 26, seed: int = 20190520):
 
     rng = np.random.default_rng(seed)
     pts = rng.random((npts, 3))
-    dist, nbr = cKDTree(pts).query(pts, k=k + 1)
-    r = np.repeat(np.arange(npts, dtype=np.int64), k)
-    c = nbr[:, 1:].ravel().astype(np.int64)
-    d = dist[:, 1:].ravel()
-    # symmetric union of the directed edges, weight 1/distance
-    rr = np.concatenate([r, c])
-    cc = np.concatenate([c, r])
-    ww = 1.0 / np.concatenate([d, d])
-    key = rr * npts + cc
-    key, first = np.unique(key, return_index=True)
-    rr, cc, ww = rr[first], cc[first], ww[first]
-    W = sp.csr_matrix((ww, (rr, cc)), shape=(npts, npts))
+    dist, nbr = cKDTree(pts).query(pts, k=k + 1, workers=-1)
+    # symmetric union of the directed edges, weight 1/distance (both
+    # directions carry the same rounded distance, so max() is the union)
+    indptr = np.arange(0, npts * k + 1, k, dtype=np.int64)
+    Wd = sp.csr_matrix((1.0 / dist[:, 1:].ravel(), nbr[:, 1:].ravel().astype(np.int64), indptr),
+                       shape=(npts, npts))
+    del dist, nbr
+    Wd.sort_indices()
+    W = Wd.maximum(Wd.T.tocsr()).tocsr()
+    del Wd
     W.sort_indices()
     deg = np.asarray(W.sum(axis=1)).ravel()
     A = (sp.diags(deg + 1e-3) - W).tocsr()

@@ -115,6 +115,31 @@ def test_mapped_and_hash_numeric_paths_agree():
     assert row_scaled_err(c_map.row_offsets, c_map.values, c_hash.values) <= 1e-15
 
 
+def test_interned_maps_shrink_plan_and_match_private_maps():
+    """Rows of one structural class share one interned slot/position map:
+    the plan keeps a fraction of the per-row map bytes, and C equals the C of
+    a plan with a private map per row (PTAP_NO_INTERN=1)."""
+    A, P = _cfg3(32)
+    ctx = pk.single_rank_context()
+
+    def one():
+        a, p = pk.distribute(A, P, 1, 0)
+        plan = pk.run_symbolic(a, p, "allatonce", ctx)
+        loc = pk.run_numeric(a, p, plan, ctx)
+        return loc.diag.row_offsets.copy(), loc.diag.col_indices.copy(), loc.diag.values.copy(), \
+            plan.memory()["current"]["plan_cache"]
+
+    ip, j, v, shared = one()
+    os.environ["PTAP_NO_INTERN"] = "1"
+    try:
+        ip2, j2, v2, private = one()
+    finally:
+        del os.environ["PTAP_NO_INTERN"]
+    assert np.array_equal(ip, ip2) and np.array_equal(j, j2)
+    assert row_scaled_err(ip, v, v2) <= 1e-15
+    assert shared < 0.5 * private, (shared, private)
+
+
 def test_device_generators_match_host_generators():
     import torch
     from paper_1905_08423_b200 import devgen
