@@ -141,6 +141,9 @@ typedef struct {
     int64_t nnz_staging;
     int64_t mac_ap;                    /* multiply-adds of the A*P rows       */
     int64_t mac_outer;                 /* multiply-adds of the outer products */
+    int64_t numeric_path;              /* all-at-once/merged numeric: 1 plan maps, 0 hash tables */
+    int64_t map_bytes;                 /* plan maps kept (slot + position pools, interned) */
+    int64_t row_structures_ppm;        /* distinct row structures per 1e6 sampled rows, -1: not sampled */
 } ptap_counters;
 
 typedef struct ptap_plan ptap_plan;

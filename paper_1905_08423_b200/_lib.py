@@ -54,7 +54,8 @@ class Counters(ctypes.Structure):
     _fields_ = [("symbolic_runs", c_i64), ("numeric_runs", c_i64),
                 ("symbolic_row_kernel_calls", c_i64), ("numeric_row_kernel_calls", c_i64),
                 ("kernel_launches", c_i64), ("nnz_c", c_i64), ("nnz_staging", c_i64),
-                ("mac_ap", c_i64), ("mac_outer", c_i64)]
+                ("mac_ap", c_i64), ("mac_outer", c_i64), ("numeric_path", c_i64), ("map_bytes", c_i64),
+                ("row_structures_ppm", c_i64)]
 
 
 ALGORITHM_CODES = {"two-step": 0, "allatonce": 1, "merged": 2}

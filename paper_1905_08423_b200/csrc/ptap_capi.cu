@@ -146,7 +146,7 @@ struct ptap_plan {
   int32_t *ct_col = nullptr;
   double *ct_val = nullptr;
   Transpose ptd, pto;
-  ptap_counters cnt{};
+  ptap_counters cnt{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1};
 };
 
 namespace {
@@ -563,6 +563,27 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   p->cnt.kernel_launches += 3;
   tr.mark(st, "  maps: maxima");
   if (h[0] > 255 || h[1] > 65535 || h[2] > 255) return PTAP_OK;  // hash path for this plan
+  // maps pay for themselves when rows repeat (interned, a small pool); on an
+  // operator whose rows do not repeat they would cost about as much memory as
+  // the two-step's auxiliary matrices, so such a plan keeps no maps and
+  // numeric runs the hash path (PTAP_MAPS=1 keeps them regardless)
+  if (!getenv("PTAP_MAPS") && p->nloc > 0) {
+    const int64_t nsample = std::min<int64_t>(p->nloc, 65536);
+    const int64_t ent = int64_t(1) << 17;
+    unsigned long long *keys = nullptr;
+    CKS(palloc(p, &keys, ent, CAT_TRANSIENT, st));
+    CK(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * ent, st));
+    CK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
+    CK(launch_struct_sample(op, nsample, keys, (unsigned long long)(ent - 1), mx, st));
+    unsigned long long distinct = 0;
+    CK(cudaMemcpyAsync(&distinct, mx, sizeof(distinct), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pfree(p, keys, st);
+    p->cnt.kernel_launches++;
+    tr.mark(st, "  maps: row-structure sample");
+    p->cnt.row_structures_ppm = (int64_t)(1e6 * (double)distinct / (double)nsample);
+    if ((int64_t)distinct * 4 > nsample) return PTAP_OK;  // rows do not repeat: hash path
+  }
   {
     // bin 0 through k_outer_numeric_q4: <= 128 map bytes per row and every
     // offset it touches within 32 bits
@@ -683,10 +704,12 @@ ptap_status intern_map(ptap_plan *p, uint8_t *&src, int64_t *&src_rp, int64_t n,
   CKS(palloc(p, &words, n, CAT_TRANSIENT, st));
   CKS(palloc(p, &wpos, n + 1, CAT_TRANSIENT, st));
   CKS(palloc(p, &scratch, scan_scratch_elems(n), CAT_TRANSIENT, st));
+  unsigned long long *claims = p->d_u64 + 20;
   CK(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * ent, st));
+  CK(cudaMemsetAsync(claims, 0, sizeof(unsigned long long), st));
   CK(launch_intern(0, n, src, src_rp, keys, vals, (unsigned long long)(ent - 1), slot_of, owner, words, nullptr,
-                   nullptr, 0, st));
-  CK(launch_intern(1, n, src, src_rp, keys, vals, 0, slot_of, owner, words, nullptr, nullptr, 0, st));
+                   nullptr, 0, claims, st));
+  CK(launch_intern(1, n, src, src_rp, keys, vals, 0, slot_of, owner, words, nullptr, nullptr, 0, claims, st));
   pfree(p, keys, st);
   pfree(p, vals, st);
   pfree(p, slot_of, st);
@@ -694,11 +717,30 @@ ptap_status intern_map(ptap_plan *p, uint8_t *&src, int64_t *&src_rp, int64_t n,
   int64_t nw = 0;
   CK(cudaMemcpyAsync(&nw, wpos + n, sizeof(nw), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  p->cnt.kernel_launches += 3;
+  if (nw * 4 > total / 2) {
+    // the rows hardly repeat (unstructured input): keep the per-row maps as
+    // they are rather than hold a second copy of most of them
+    pfree(p, owner, st);
+    pfree(p, words, st);
+    pfree(p, wpos, st);
+    pfree(p, scratch, st);
+    if (pack_len) {
+      CKS(palloc(p, &out, n + 1, CAT_PLAN, st));
+      CK(launch_pack_offsets(n, src_rp, out, st));
+      p->cnt.kernel_launches++;
+      pfree(p, src_rp, st);
+      src_rp = out;
+    }
+    *pool_bytes = total;
+    return PTAP_OK;
+  }
   uint8_t *pool = nullptr;
   CKS(palloc(p, &pool, nw * 4 + 16, CAT_PLAN, st));  // +16: the numeric kernels stage maps as words
   CKS(palloc(p, &out, n + 1, CAT_PLAN, st));
-  CK(launch_intern(2, n, src, src_rp, nullptr, nullptr, 0, nullptr, owner, wpos, pool, out, pack_len ? 1 : 0, st));
-  p->cnt.kernel_launches += 4;
+  CK(launch_intern(2, n, src, src_rp, nullptr, nullptr, 0, nullptr, owner, wpos, pool, out, pack_len ? 1 : 0,
+                   nullptr, st));
+  p->cnt.kernel_launches++;
   pfree(p, owner, st);
   pfree(p, words, st);
   pfree(p, wpos, st);
@@ -741,6 +783,8 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
       CKS(intern_map(p, p->maps.smap, p->maps.smap_rp, p->nloc, p->smap_bytes, true, &p->smap_bytes, st));
     p->smap_interned = true;
     CKS(intern_map(p, p->maps.pmap, p->maps.pmap_rp, p->nloc, p->pmap_bytes, false, &p->pmap_bytes, st));
+    p->cnt.numeric_path = 1;
+    p->cnt.map_bytes = p->smap_bytes + p->pmap_bytes;
   }
   if (!ok) {
     pfree(p, p->maps.smap_rp, st);

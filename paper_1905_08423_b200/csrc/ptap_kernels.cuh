@@ -156,10 +156,12 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
                                         int *status, cudaStream_t st, int row0 = 0);
 cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, const MapArgs &mp,
                                      const OuterTargets &tg, int *status, cudaStream_t st, int row0 = 0);
+cudaError_t launch_struct_sample(const Ops &op, int64_t nsample, unsigned long long *keys, unsigned long long mask,
+                                 unsigned long long *distinct, cudaStream_t st);
 cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cudaStream_t st);
 cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t *src_rp, unsigned long long *keys,
                           int64_t *vals, unsigned long long mask, int64_t *slot_of, int64_t *owner, int64_t *words,
-                          uint8_t *pool, int64_t *out, int pack_len, cudaStream_t st);
+                          uint8_t *pool, int64_t *out, int pack_len, unsigned long long *claims, cudaStream_t st);
 // packed smap_rp entries of an interned plan: pool offset | map length << 40
 constexpr unsigned long long SMAP_OFF_MASK = (1ull << 40) - 1;
 cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,

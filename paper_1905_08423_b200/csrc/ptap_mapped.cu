@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -771,7 +772,8 @@ __device__ __forceinline__ unsigned long long intern_hash(const uint8_t *s, int 
 
 __global__ void __launch_bounds__(256) k_intern_claim(int64_t n, const uint8_t *src, const int64_t *src_rp,
                                                       unsigned long long *keys, int64_t *vals,
-                                                      unsigned long long mask, int64_t *slot_of) {
+                                                      unsigned long long mask, int64_t *slot_of,
+                                                      unsigned long long *claims) {
   constexpr int G = INTERN_G;
   const int lane = lane_id(), gl = lane & (G - 1);
   const unsigned gmask = 0xffu << (lane & ~(G - 1));
@@ -790,8 +792,15 @@ __global__ void __launch_bounds__(256) k_intern_claim(int64_t n, const uint8_t *
       for (int probe = 0; probe < INTERN_PROBES; ++probe) {
         unsigned long long k = keys[slot];  // a stale 0 only costs a CAS
         if (k == 0) {
+          // claims stop at half the table (rows that do not repeat -- an
+          // unstructured input -- must not fill it): later new strings
+          // stay private
+          if (*(volatile unsigned long long *)claims > (mask >> 1)) break;
           k = atomicCAS(keys + slot, 0ull, h);
-          if (k == 0) vals[slot] = i;  // the representative; read after this kernel
+          if (k == 0) {
+            vals[slot] = i;  // the representative; read after this kernel
+            atomicAdd(claims, 1ull);
+          }
         }
         if (k == 0 || k == h) { found = (int64_t)slot; break; }
         slot = (slot + 1) & mask;
@@ -851,6 +860,78 @@ __global__ void __launch_bounds__(256) k_intern_copy(int64_t n, const uint8_t *s
   }
 }
 
+// ---------------------------------------------------------------------------
+// Do the rows repeat?  A fine row's slot map is fixed by its A row length, the
+// P row lengths of its columns and the relative order of the pairs' coarse
+// columns, so rows whose (length, P row lengths, column - row minimum)
+// sequences agree share their slot map.  k_struct_sample hashes that
+// signature for a pseudo-random sample of rows (a warp per row) and counts the
+// distinct ones in a table; the plan keeps interned maps only when the sample
+// repeats (structured operators), and unstructured operators take the hash
+// numeric path, which stores nothing per row.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sig_row_block(const Ops &op, int src, int64_t i, int &lo, unsigned long long &h,
+                                              bool hash_pass) {
+  const int lane = lane_id();
+  const int64_t *arp = src ? op.ao_rp : op.ad_rp;
+  if (arp == nullptr) return;
+  const int32_t *acol = src ? op.ao_col : op.ad_col;
+  const int64_t *qrp = src ? op.pr_rp : op.pd_rp;
+  const int32_t *qcol = src ? op.pr_col : op.pd_col;
+  const int32_t coff = src ? 0 : (int32_t)op.c_lo;
+  const bool po_here = src == 0 && op.po_rp != nullptr;
+  const int64_t t0 = arp[i], t1 = arp[i + 1];
+  for (int64_t t = t0 + lane; t < t1; t += 32) {
+    const int32_t k = acol[t];
+    const int64_t d0 = qrp[k], d1 = qrp[k + 1];
+    const int64_t o0 = po_here ? op.po_rp[k] : 0, o1 = po_here ? op.po_rp[k + 1] : 0;
+    unsigned long long he = 0;
+    for (int64_t q = d0; q < d1 + (o1 - o0); ++q) {
+      const int32_t g = q < d1 ? qcol[q] + coff : op.p_colmap[op.po_col[o0 + (q - d1)]];
+      if (!hash_pass) lo = min(lo, g);
+      else he += mix64(((unsigned long long)(q - d0) << 32) | (uint32_t)(g - lo));
+    }
+    if (hash_pass)
+      h += mix64(he ^ ((unsigned long long)(src * 4096 + (t - t0)) << 40) ^ ((unsigned long long)(d1 - d0 + o1 - o0) << 56));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_struct_sample(Ops op, int64_t nsample, unsigned long long *keys,
+                                                       unsigned long long mask, unsigned long long *distinct) {
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nsample; j += nw) {
+    const int64_t i = nsample >= op.nloc ? j : (int64_t)(mix64((unsigned long long)j) % (unsigned long long)op.nloc);
+    int lo = INT_MAX;
+    unsigned long long h = 0;
+    for (int src = 0; src < 2; ++src) sig_row_block(op, src, i, lo, h, false);
+    lo = __reduce_min_sync(FULL, lo);
+    for (int src = 0; src < 2; ++src) sig_row_block(op, src, i, lo, h, true);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(FULL, h, o);
+    const int64_t alen = (op.ad_rp[i + 1] - op.ad_rp[i]) + (op.ao_rp ? op.ao_rp[i + 1] - op.ao_rp[i] : 0);
+    h = mix64(h ^ (unsigned long long)alen);
+    if (h == 0) h = 1;
+    if (lane == 0) {
+      unsigned long long slot = h & mask;
+      for (int probe = 0; probe <= (int)mask; ++probe) {
+        const unsigned long long k = atomicCAS(keys + slot, 0ull, h);
+        if (k == 0) { atomicAdd(distinct, 1ull); break; }
+        if (k == h) break;
+        slot = (slot + 1) & mask;
+      }
+    }
+  }
+}
+
+cudaError_t launch_struct_sample(const Ops &op, int64_t nsample, unsigned long long *keys, unsigned long long mask,
+                                 unsigned long long *distinct, cudaStream_t st) {
+  if (nsample <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((nsample + 7) / 8, 148 * 16);
+  k_struct_sample<<<blocks, 256, 0, st>>>(op, nsample, keys, mask, distinct);
+  return cudaGetLastError();
+}
+
 __global__ void k_pack_offsets(int64_t n, const int64_t *rp, int64_t *out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = rp[i] | ((rp[i + 1] - rp[i]) << 40);
@@ -863,10 +944,10 @@ cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cuda
 
 cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t *src_rp, unsigned long long *keys,
                           int64_t *vals, unsigned long long mask, int64_t *slot_of, int64_t *owner, int64_t *words,
-                          uint8_t *pool, int64_t *out, int pack_len, cudaStream_t st) {
+                          uint8_t *pool, int64_t *out, int pack_len, unsigned long long *claims, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((n + 31) / 32, 148 * 32);
-  if (pass == 0) k_intern_claim<<<blocks, 256, 0, st>>>(n, src, src_rp, keys, vals, mask, slot_of);
+  if (pass == 0) k_intern_claim<<<blocks, 256, 0, st>>>(n, src, src_rp, keys, vals, mask, slot_of, claims);
   else if (pass == 1) k_intern_resolve<<<blocks, 256, 0, st>>>(n, src, src_rp, vals, slot_of, owner, words);
   else k_intern_copy<<<blocks, 256, 0, st>>>(n, src, src_rp, owner, words, pool, out, pack_len);
   return cudaGetLastError();

@@ -93,3 +93,36 @@ def test_gpu_parity_amg_inputs(which, nr, alg, request):
     if alg == "two-step":
         assert np.array_equal(c.values.view(np.uint64), want.val.view(np.uint64))
     assert row_scaled_err(want.row_ptr, c.values, want.val) <= TOL
+
+
+@pytest.mark.gpu
+def test_map_policy_structured_vs_unstructured(cfg5_large):
+    """Plan maps are kept when sampled rows repeat (a stencil: a handful of
+    structural classes) and skipped when they do not (the kNN graph): that
+    plan runs the hash numeric path and keeps no per-row maps.  Forcing maps
+    (PTAP_MAPS=1) on the unstructured input gives the same C."""
+    import os
+
+    import paper_1905_08423_b200 as pk
+    from oracle.oracle import oracle_ptap
+    from paper_1905_08423_b200 import problems as gen
+
+    ctx = pk.single_rank_context()
+    A3, P3 = gen.config_operands(gen.CONFIGS["cfg3"], n_fine=24)
+    for (A, P), path in (((A3, P3), 1), (cfg5_large, 0)):
+        a, p = pk.distribute(A, P, 1, 0)
+        plan = pk.run_symbolic(a, p, "allatonce", ctx)
+        d = plan.device_counters()
+        assert d["numeric_path"] == path, d
+        assert (d["map_bytes"] > 0) == (path == 1)
+        assert 0 <= d["row_structures_ppm"] <= 10 ** 6
+    A, P = cfg5_large
+    want = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values, P.row_offsets,
+                       P.col_indices, P.values, nranks=1, algorithm="allatonce")
+    os.environ["PTAP_MAPS"] = "1"
+    try:
+        c, _ = run_ptap(A, P, 1, "allatonce")
+    finally:
+        del os.environ["PTAP_MAPS"]
+    assert np.array_equal(c.row_offsets, want.row_ptr) and np.array_equal(c.col_indices, want.col)
+    assert row_scaled_err(want.row_ptr, c.values, want.val) <= TOL

@@ -106,7 +106,9 @@ def measure(a, p, reps, ctx):
              "ptap_wall_ms": sym * 1e3 + ms, "gflops": 2.0 * mac / (ms * 1e-3) / 1e9,
              "alg_gbs": alg_b / (ms * 1e-3) / 1e9, "roofline_frac": alg_b / (ms * 1e-3) / 1e9 / peak,
              "aux_peak_bytes": mem["device_high_water"] - mem["current"]["output_matrix"],
-             "plan_cache_bytes": mem["current"]["plan_cache"], "mac": mac, "nnz_c": int(c_col.numel())}
+             "plan_cache_bytes": mem["current"]["plan_cache"], "mac": mac, "nnz_c": int(c_col.numel()),
+             "numeric_path": ("plan maps" if cnt["numeric_path"] else "hash") if alg != "two-step" else "two-step",
+             "map_bytes": cnt["map_bytes"], "row_structures_ppm": cnt["row_structures_ppm"]}
         if ref is None:
             ref = (c_rp.clone(), c_col.clone(), c_val.clone())
         else:
