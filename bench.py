@@ -460,7 +460,7 @@ def our_arm(args):
                        "gen_s": gen_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_outer_numeric_q4 (ptap_numeric_local)", "kernel_ms": kms,
+                         "kernel": "k_outer_numeric_q4a (ptap_numeric_local)", "kernel_ms": kms,
                          "alg_bytes_per_launch": my_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
