@@ -90,6 +90,9 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_MINB_Q4A
 #define PTAP_MINB_Q4A 4
 #endif
+#ifndef PTAP_QA_PF
+#define PTAP_QA_PF 1
+#endif
 // per-group shared region: accumulator (NAPCAP + 1 slots), then G step
 // entries and G P_o row starts (group stride 352 B for <4,32>: successive
 // groups start 12 bank pairs apart -- the best of the strides measured)
@@ -619,9 +622,36 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
     // fold: A entries from shared memory, P values and row bounds from global
     int run = 0;
     const int maxlen = __reduce_max_sync(FULL, len);
+#if PTAP_QA_PF
+    // the next chunk's A value and P row bounds are loaded while this
+    // chunk's steps run (the column -> row-bounds chain is the top stall)
+    int nd0 = 0, nd1 = 0;
+    double na = 0.0;
+    auto fetch = [&](int tt) {
+      nd0 = nd1 = 0;
+      na = 0.0;
+      if (tt < len) {
+        const int k = S.col[t0 + tt];
+        na = __ldg(op.ad_val + a0 + t0 + tt);
+        if (mp.poff) {
+          nd0 = k & 0x0fffffff;
+          nd1 = nd0 + (int)((unsigned)k >> 28);
+        } else {
+          nd0 = (int)__ldg(op.pd_rp + k);
+          nd1 = (int)__ldg(op.pd_rp + k + 1);
+        }
+      }
+    };
+    fetch(gl);
+#endif
 #pragma unroll 1
     for (int tb = 0; tb < maxlen; tb += G) {
       const int t = tb + gl;
+#if PTAP_QA_PF
+      const double a = na;
+      const int d0 = nd0, plen = nd1 - nd0;
+      fetch(t + G);
+#else
       double a = 0.0;
       int d0 = 0, plen = 0;
       if (t < len) {
@@ -639,6 +669,7 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
           plen = (int)__ldg(op.pd_rp + k + 1) - d0;
         }
       }
+#endif
       int incl = plen;
 #pragma unroll
       for (int o = 1; o < G; o <<= 1) {
