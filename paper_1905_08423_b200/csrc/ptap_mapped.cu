@@ -93,6 +93,12 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_QA_PF
 #define PTAP_QA_PF 1
 #endif
+#ifndef PTAP_QA_PRED
+#define PTAP_QA_PRED 1
+#endif
+#ifndef PTAP_QA_PRED_OUTER
+#define PTAP_QA_PRED_OUTER 0
+#endif
 // per-group shared region: accumulator (NAPCAP + 1 slots), then G step
 // entries and G P_o row starts (group stride 352 B for <4,32>: successive
 // groups start 12 bank pairs apart -- the best of the strides measured)
@@ -498,6 +504,51 @@ static unsigned long long resident(K kern, int threads, size_t smem) {
 
 static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 
+// 32-bit shared-window accesses and predicated loads/stores for the q4a
+// fold: without them ptxas rematerialises the accumulator's shared-window
+// base (S2R SR_CgaCtaId) and a global-memory descriptor for every step under
+// the 64-register budget, and wraps each conditional access in a divergent
+// region (BSSY/BSYNC)
+__device__ __forceinline__ uint32_t sh_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int2 lds_v2s32(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64_if(bool p, uint32_t a) {
+  double v = 0.0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}" : "+d"(v) : "r"(a), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8_if(bool p, uint32_t a) {
+  uint32_t v = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u8 %0, [%1];\n}" : "+r"(v) : "r"(a), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ void sts_f64_if(bool p, uint32_t a, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}" ::"r"(a), "d"(v), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ldg_u8_if(bool p, const uint8_t *ptr) {
+  uint32_t v = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.u8 %0, [%1];\n}" : "+r"(v) : "l"(ptr), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ void red_add_f64_if(bool p, double *ptr, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q red.global.add.f64 [%0], %1;\n}" ::"l"(ptr), "d"(v), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ double ldg_f64_if(bool p, const double *ptr) {
+  double v = 0.0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}" : "+d"(v) : "l"(ptr), "r"((int)p));
+  return v;
+}
+
 // q4a outer phase with the C-row-start map: every lane of a row's group reads
 // each target's (C row start, P value) directly (one broadcast load each, two
 // targets in flight), no shuffles, no column -> row-pointer chain
@@ -512,6 +563,23 @@ __device__ __forceinline__ void outer_scatter_cb(const Ops &op, const MapArgs &m
     double v0 = 0.0, v1 = 0.0;
     if (jj < nP) { b0 = __ldg(mp.cbase + pd0 + jj); v0 = __ldg(op.pd_val + pd0 + jj); }
     if (jj + 1 < nP) { b1 = __ldg(mp.cbase + pd0 + jj + 1); v1 = __ldg(op.pd_val + pd0 + jj + 1); }
+#if PTAP_QA_PRED_OUTER
+    // predicated, branch-free: per slot one byte load and one reduction
+    // (measured slower: 7.35 vs 7.21 ms; off)
+    {
+      const uint8_t *pm0 = mp.pmap + pbase + (int64_t)jj * nap;
+      const uint8_t *pm1 = pm0 + nap;
+      double *c0 = tg.c_val + (b0 >= 0 ? b0 : 0), *c1 = tg.c_val + (b1 >= 0 ? b1 : 0);
+#pragma unroll
+      for (int k = 0; k < NREG; ++k) {
+        const int s = gl + G * k;
+        const bool p0 = b0 >= 0 && s < nap, p1 = b1 >= 0 && s < nap;
+        const uint32_t q0 = ldg_u8_if(p0, pm0 + s), q1 = ldg_u8_if(p1, pm1 + s);
+        red_add_f64_if(p0, c0 + q0, __dmul_rn(v0, accr[k]));
+        red_add_f64_if(p1, c1 + q1, __dmul_rn(v1, accr[k]));
+      }
+    }
+#else
     if (b0 >= 0) {
       const uint8_t *pm = mp.pmap + pbase + (int64_t)jj * nap;
 #pragma unroll
@@ -528,6 +596,7 @@ __device__ __forceinline__ void outer_scatter_cb(const Ops &op, const MapArgs &m
         if (s < nap) atomicAdd(tg.c_val + b1 + __ldg(pm + s), __dmul_rn(v1, accr[k]));
       }
     }
+#endif
   }
 }
 
@@ -598,6 +667,9 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
   Q4Warp &W = ((Q4Warp *)((double *)smem + nwarps * Q4_RPW * Q4_ACC))[warp];
   QaStage &S = ((QaStage *)((unsigned char *)smem + nwarps * (Q4_RPW * Q4_ACC * sizeof(double) + sizeof(Q4Warp))))[warp];
   const uint8_t *smb = (const uint8_t *)W.sm;
+#if PTAP_QA_PRED
+  const uint32_t acc_sa = sh_addr(acc), smb_sa = sh_addr(smb), dp_sa = sh_addr(&W.dp[0][r]), a_sa = sh_addr(&W.a[0][r]);
+#endif
   const int total = row0 + (int)nrows;
   const int stride = gridDim.x * nwarps * Q4_RPW;
   int r0 = row0 + (blockIdx.x * nwarps + warp) * Q4_RPW;
@@ -681,6 +753,41 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
       run += __shfl_sync(FULL, incl, G - 1, G);
       __syncwarp();
       const int steps = min(G, maxlen - tb);
+#if PTAP_QA_PRED
+      double pv[G];
+      uint32_t sv[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int2 e = lds_v2s32(dp_sa + j * (Q4_RPW * 8));
+        const bool act = j < steps && gl < (int)((uint32_t)e.y >> 24);
+        pv[j] = ldg_f64_if(act, op.pd_val + (uint32_t)(e.x + gl));
+        sv[j] = lds_u8_if(act, smb_sa + (uint32_t)(sbo + (e.y & 0xffff) + gl));
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        if (j < steps) {
+          const int2 e = lds_v2s32(dp_sa + j * (Q4_RPW * 8));
+          const int plj = (int)((uint32_t)e.y >> 24);
+          const bool act = gl < plj;
+          const double aj = lds_f64(a_sa + j * (Q4_RPW * 8));
+          const uint32_t s = sv[j], ad = acc_sa + (s & 0x7f) * 8;
+          const double prod = __dmul_rn(aj, pv[j]);
+          const double old = lds_f64_if(act && !(s & 0x80), ad);
+          sts_f64_if(act, ad, (s & 0x80) ? prod : __dadd_rn(old, prod));
+          if (plj > G) {  // P rows longer than the group (rare)
+            const uint32_t off = smb_sa + (uint32_t)(sbo + (e.y & 0xffff));
+            for (int u = gl + G; u < plj; u += G) {
+              const double pu = __ldg(op.pd_val + (uint32_t)(e.x + u));
+              const uint32_t s2 = lds_u8_if(true, off + u), ad2 = acc_sa + (s2 & 0x7f) * 8;
+              const double pr2 = __dmul_rn(aj, pu);
+              const double old2 = lds_f64_if(!(s2 & 0x80), ad2);
+              sts_f64_if(true, ad2, (s2 & 0x80) ? pr2 : __dadd_rn(old2, pr2));
+            }
+          }
+          __syncwarp();
+        }
+      }
+#else
       double pv[G];
       int sv[G];
 #pragma unroll
@@ -718,6 +825,7 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
           __syncwarp();
         }
       }
+#endif
     }
     __syncwarp();
     // the next batch's A entries and slot maps stream in behind the scatter
@@ -725,7 +833,11 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
     const int nap = i >= 0 ? (int)__ldg(mp.nap + i) : 0;
     double accr[NREG];
 #pragma unroll
+#if PTAP_QA_PRED_OUTER
+    for (int q = 0; q < NREG; ++q) accr[q] = lds_f64_if(gl + G * q < nap, acc_sa + (gl + G * q) * 8);
+#else
     for (int q = 0; q < NREG; ++q) accr[q] = (gl + G * q < nap) ? acc[gl + G * q] : 0.0;
+#endif
     if (mp.cbase)
       outer_scatter_cb<G, NREG>(op, mp, tg, i, pd0, pd1, nap, accr, gl);
     else
