@@ -896,7 +896,9 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
     for (int q = 0; q < NBINS; ++q) {
       if (bs.count[q] == 0) continue;
       const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
-      if (q == 0 && p->q4a && bs.identity0 && do_local && !do_send) {
+      // q4a plans have no P_o (one-rank structure), so a merged pass's send
+      // half is empty and its fused loop is the local loop
+      if (q == 0 && p->q4a && bs.identity0 && do_local && (!do_send || op.po_rp == nullptr)) {
         CK(launch_outer_numeric_q4a(op, (unsigned long long)bs.count[q], p->maps, tg, p->d_status, st, 0));
         p->cnt.kernel_launches++;
         continue;
