@@ -99,6 +99,9 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_QA_PRED_OUTER
 #define PTAP_QA_PRED_OUTER 0
 #endif
+#ifndef PTAP_QA_PERM
+#define PTAP_QA_PERM 1
+#endif
 // per-group shared region: accumulator (NAPCAP + 1 slots), then G step
 // entries and G P_o row starts (group stride 352 B for <4,32>: successive
 // groups start 12 bank pairs apart -- the best of the strides measured)
@@ -315,7 +318,10 @@ __global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_m
 // shared memory with one coalesced sweep instead of 8 row-strided byte
 // gathers per step, and the step entries live in [step][row] arrays so each
 // per-step broadcast is a single conflict-free 8-byte load.
-constexpr int Q4_RPW = 8, Q4_G = 4, Q4_CAP = 32, Q4_ACC = 36, Q4_SMW = 264;
+#ifndef PTAP_Q4_ACC
+#define PTAP_Q4_ACC 36
+#endif
+constexpr int Q4_RPW = 8, Q4_G = 4, Q4_CAP = 32, Q4_ACC = PTAP_Q4_ACC, Q4_SMW = 264;
 struct __align__(16) Q4Warp {
   double a[Q4_G][Q4_RPW];     // A value of step j, row r
   int2 dp[Q4_G][Q4_RPW];      // start of its P row, packed offsets/lengths
@@ -632,6 +638,18 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// row of a batch handled by lane group g: with PTAP_QA_PERM the first
+// half-warp takes the batch's even rows and the second its odd rows, so on a
+// lexicographic grid (x parity alternating) each half-warp folds rows of one
+// structural class, whose same-step slots sit at fixed bank offsets
+__device__ __forceinline__ int qa_row(int g) {
+#if PTAP_QA_PERM
+  return ((g & 3) << 1) | (g >> 2);
+#else
+  return g;
+#endif
+}
+
 // issue the copies of batch [r0, r0 + 8) (rows are consecutive)
 __device__ __forceinline__ void qa_stage(const Ops &op, const MapArgs &mp, Q4Warp &W, QaStage &S, int r0, int total,
                                          int lane) {
@@ -646,7 +664,7 @@ __device__ __forceinline__ void qa_stage(const Ops &op, const MapArgs &mp, Q4War
   }
   // slot maps row by row: rows of one class share an interned map, so a
   // batch's maps are not one contiguous run
-  const int i = r0 + (lane >> 2);
+  const int i = r0 + qa_row(lane >> 2);
   if (i < r1) {
     const unsigned long long sx = __ldg(mp.smap_rp + i);
     const int sb = (int)(sx & SMAP_OFF_MASK), slen = (int)(sx >> 40);
@@ -675,7 +693,7 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
   int r0 = row0 + (blockIdx.x * nwarps + warp) * Q4_RPW;
   if (r0 < total) qa_stage(op, mp, W, S, r0, total, lane);
   for (; r0 < total; r0 += stride) {
-    const int i_all = r0 + r;
+    const int i_all = r0 + qa_row(r);
     int i = i_all < total ? i_all : -1;
     int pd0 = 0, pd1 = 0;
     if (i >= 0) { pd0 = (int)__ldg(op.pd_rp + i); pd1 = (int)__ldg(op.pd_rp + i + 1); }
