@@ -343,12 +343,12 @@ def our_arm(args):
     import gc
 
     def warm_symbolic(alg):
-        """cold call (one-time module and memory-pool setup), then two warm
-        calls; the warm figure is the faster of the two (the host-side driver
-        calls occasionally stall for ~0.1 s on these boxes)"""
+        """cold call (one-time module and memory-pool setup), then three warm
+        calls; the warm figure is the fastest (the host-side driver calls
+        occasionally stall for tens of ms on these boxes; all are reported)"""
         pl, cold = symbolic(alg)
         warm = []
-        for _ in range(2):
+        for _ in range(3):
             del pl
             gc.collect()
             torch.cuda.synchronize()
