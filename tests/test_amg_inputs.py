@@ -126,3 +126,22 @@ def test_map_policy_structured_vs_unstructured(cfg5_large):
         del os.environ["PTAP_MAPS"]
     assert np.array_equal(c.row_offsets, want.row_ptr) and np.array_equal(c.col_indices, want.col)
     assert row_scaled_err(want.row_ptr, c.values, want.val) <= TOL
+
+
+def test_greedy_aggregation_compiled_matches_reference_loops():
+    """The numba-compiled aggregation (used at config-5 scale) gives the same
+    aggregates as the numpy restatement of the two passes."""
+    import scipy.sparse as sp
+    from scipy.spatial import cKDTree
+
+    rng = np.random.default_rng(7)
+    pts = rng.random((4000, 3))
+    _, nb = cKDTree(pts).query(pts, k=9)
+    r = np.repeat(np.arange(4000), 8)
+    W = sp.csr_matrix((np.ones(r.size), (r, nb[:, 1:].ravel())), shape=(4000, 4000))
+    W = (W + W.T).tocsr()
+    W.sort_indices()
+    a = amg._greedy_aggregate_py(W.indptr, W.indices, 4000)
+    b = amg._greedy_aggregate(W.indptr, W.indices, 4000)
+    assert np.array_equal(a, b)
+    assert a.min() == 0 and np.all(np.diff(np.unique(a)) == 1)
