@@ -856,10 +856,14 @@ __global__ void __launch_bounds__(256, PTAP_MINB_Q4A) k_outer_numeric_q4a(Ops op
 #else
     for (int q = 0; q < NREG; ++q) accr[q] = (gl + G * q < nap) ? acc[gl + G * q] : 0.0;
 #endif
+#ifdef PTAP_QA_ABLATE_OUTER  // timing experiments only: C is not written
+    if (accr[0] == 1.2345e-300) tg.c_val[0] = accr[1];
+#else
     if (mp.cbase)
       outer_scatter_cb<G, NREG>(op, mp, tg, i, pd0, pd1, nap, accr, gl);
     else
       outer_scatter<G, NREG>(op, mp, tg, i, pd0, pd1, 0, 0, wl, false, nap, accr, gl);
+#endif
   }
   cp_async_wait_all();
 }
