@@ -115,6 +115,7 @@ struct ptap_plan {
   bool q4_sym = false;              // ... and k_outer_symbolic_q4
   bool pmap_ready = false;          // position maps written by the row-union pass
   bool smap_interned = false;       // slot maps already interned (row-union path)
+  bool rows_unstructured = false;   // sampled row structures do not repeat
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
   bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
   double avg_p_row = 4.0;           // P entries per local fine row (arena sizing)
@@ -543,6 +544,29 @@ ptap_status with_arena_retry(ptap_plan *p, Arena &ar, cudaStream_t st, F pass) {
   return fail(PTAP_ERR_OOM, "symbolic arena kept overflowing");
 }
 
+// Do the operator's rows repeat structurally?  k_struct_sample counts the
+// distinct row signatures of 65,536 sampled rows; more than one in four
+// distinct marks the operator unstructured (maps are skipped, rows are
+// visited in aggregate order).
+ptap_status sample_row_structures(ptap_plan *p, const Ops &op, cudaStream_t st) {
+  if (p->nloc <= 0) return PTAP_OK;
+  const int64_t nsample = std::min<int64_t>(p->nloc, 65536);
+  const int64_t ent = int64_t(1) << 17;
+  unsigned long long *keys = nullptr, *cnt = p->d_u64 + 21;
+  CKS(palloc(p, &keys, ent, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * ent, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+  CK(launch_struct_sample(op, nsample, keys, (unsigned long long)(ent - 1), cnt, st));
+  unsigned long long distinct = 0;
+  CK(cudaMemcpyAsync(&distinct, cnt, sizeof(distinct), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  pfree(p, keys, st);
+  p->cnt.kernel_launches++;
+  p->cnt.row_structures_ppm = (int64_t)(1e6 * (double)distinct / (double)nsample);
+  p->rows_unstructured = (int64_t)distinct * 4 > nsample;
+  return PTAP_OK;
+}
+
 // Plan-mapped numeric: byte maps of slots (AP row) and positions (target rows)
 // computed once here so numeric passes do no hashing and no searching.
 // Plan-mapped numeric, part 1 (before the outer-product symbolic pass): the
@@ -567,23 +591,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   // operator whose rows do not repeat they would cost about as much memory as
   // the two-step's auxiliary matrices, so such a plan keeps no maps and
   // numeric runs the hash path (PTAP_MAPS=1 keeps them regardless)
-  if (!getenv("PTAP_MAPS") && p->nloc > 0) {
-    const int64_t nsample = std::min<int64_t>(p->nloc, 65536);
-    const int64_t ent = int64_t(1) << 17;
-    unsigned long long *keys = nullptr;
-    CKS(palloc(p, &keys, ent, CAT_TRANSIENT, st));
-    CK(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * ent, st));
-    CK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
-    CK(launch_struct_sample(op, nsample, keys, (unsigned long long)(ent - 1), mx, st));
-    unsigned long long distinct = 0;
-    CK(cudaMemcpyAsync(&distinct, mx, sizeof(distinct), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    pfree(p, keys, st);
-    p->cnt.kernel_launches++;
-    tr.mark(st, "  maps: row-structure sample");
-    p->cnt.row_structures_ppm = (int64_t)(1e6 * (double)distinct / (double)nsample);
-    if ((int64_t)distinct * 4 > nsample) return PTAP_OK;  // rows do not repeat: hash path
-  }
+  if (!getenv("PTAP_MAPS") && p->rows_unstructured) return PTAP_OK;  // rows do not repeat: hash path
   {
     // bin 0 through k_outer_numeric_q4: <= 128 map bytes per row and every
     // offset it touches within 32 bits
@@ -890,6 +898,28 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
   return ret;
 }
 
+// each bin's row list in locality order (launch_row_order); an identity bin
+// becomes an explicit list
+ptap_status order_bins(ptap_plan *p, BinSet &bs, const Ops &op, cudaStream_t st) {
+  for (int q = 0; q < NBINS; ++q) {
+    const int64_t n = bs.count[q];
+    if (n < 2) continue;
+    const bool ident = q == 0 && bs.identity0;
+    int32_t *out = nullptr;
+    CKS(palloc(p, &out, n, CAT_PLAN, st));
+    const size_t bytes = row_order_scratch_bytes(n);
+    uint8_t *scratch = nullptr;
+    CKS(palloc(p, &scratch, (int64_t)bytes, CAT_TRANSIENT, st));
+    CK(launch_row_order(n, ident ? nullptr : bs.rows[q], out, op.pd_rp, op.pd_col, scratch, bytes, st));
+    p->cnt.kernel_launches += 2;
+    pfree(p, scratch, st);
+    if (!ident) pfree(p, bs.rows[q], st);
+    bs.rows[q] = out;
+    if (ident) bs.identity0 = false;
+  }
+  return PTAP_OK;
+}
+
 ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_send, int do_local, cudaStream_t st) {
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   if (p->mapped) {
@@ -993,6 +1023,8 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   if (p->nloc > 0) p->avg_p_row = (double)(ops->p_diag.nnz + ops->p_off.nnz) / (double)p->nloc;
   CKS(ap_sizes(p, op, &p->ap_nnz, st, &p->apub));
   tr.mark(st, "ap_sizes");
+  CKS(sample_row_structures(p, op, st));
+  tr.mark(st, "row-structure sample");
   if (p->alg != PTAP_TWO_STEP) CKS(prepare_maps(p, op, ops, st));
   tr.mark(st, "prepare_maps");
   if (p->alg == PTAP_TWO_STEP) {
@@ -1191,6 +1223,14 @@ c_allocated:
   tr.mark(st, "merge slots / two-step bins");
   if (p->alg != PTAP_TWO_STEP) CKS(build_maps(p, op, ops, st));
   tr.mark(st, "position maps");
+  if (p->rows_unstructured && !(p->alg != PTAP_TWO_STEP && p->mapped) && !getenv("PTAP_NO_ROW_ORDER")) {
+    // an operator whose rows do not repeat: visit rows in aggregate order
+    // (k_row_order_keys) -- the hash numeric path, and two-step's C~ = A P
+    CKS(order_bins(p, p->bins_local, op, st));
+    CKS(order_bins(p, p->bins_all, op, st));
+    CKS(order_bins(p, p->bins_send, op, st));
+    tr.mark(st, "row order");
+  }
   pfree(p, p->ap_nnz, st);
   pfree(p, p->apub, st);
   int s = 0;

@@ -158,6 +158,9 @@ cudaError_t launch_outer_numeric_q4a(const Ops &op, unsigned long long nrows, co
                                      const OuterTargets &tg, int *status, cudaStream_t st, int row0 = 0);
 cudaError_t launch_struct_sample(const Ops &op, int64_t nsample, unsigned long long *keys, unsigned long long mask,
                                  unsigned long long *distinct, cudaStream_t st);
+size_t row_order_scratch_bytes(int64_t n);
+cudaError_t launch_row_order(int64_t n, const int32_t *rows_in, int32_t *rows_out, const int64_t *pd_rp,
+                             const int32_t *pd_col, void *scratch, size_t scratch_bytes, cudaStream_t st);
 cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cudaStream_t st);
 cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t *src_rp, unsigned long long *keys,
                           int64_t *vals, unsigned long long mask, int64_t *slot_of, int64_t *owner, int64_t *words,
