@@ -933,7 +933,8 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
         p->cnt.kernel_launches++;
         continue;
       }
-      CK(launch_outer_numeric_mapped(q == 0 ? (p->q4 ? 3 : 0) : 1, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
+      const int kb = q == 0 ? (p->q4 ? 3 : 0) : (q == 1 && !getenv("PTAP_NO_MAPPED16") ? 2 : 1);
+      CK(launch_outer_numeric_mapped(kb, op, rows, (unsigned long long)bs.count[q], p->maps, tg, do_send,
                                      do_local, p->d_status, st));
       p->cnt.kernel_launches++;
     }

@@ -1253,6 +1253,15 @@ cudaError_t launch_outer_numeric_mapped(int bin, const Ops &op, const int32_t *r
     grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
     k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
                                                                     status);
+  } else if (bin == 2) {  // AP rows of 33..128 slots: 16 lanes per row, two rows per warp
+    constexpr int G = 16, CAP = 128;
+    const int gpc = warps * (32 / G);
+    size_t sm = (size_t)gpc * group_bytes(G, CAP);
+    if ((e = opt_in(k_outer_numeric_mapped<G, CAP>, sm)) != cudaSuccess) return e;
+    unsigned long long grid = (nrows + gpc - 1) / gpc;
+    grid = std::min(grid, grid_cap(k_outer_numeric_mapped<G, CAP>, warps * 32, sm));
+    k_outer_numeric_mapped<G, CAP><<<(int)grid, warps * 32, sm, st>>>(op, rows, nrows, mp, tg, do_send, do_local,
+                                                                    status);
   } else {
     constexpr int G = 32, CAP = 256;
     const int gpc = warps;
