@@ -88,6 +88,11 @@ struct __align__(16) StepEntry {
 #ifndef PTAP_PF
 #define PTAP_PF 1
 #endif
+// resident CTAs requested for the 16-lane wide-row kernel (cfg4: 1 -> 16.8,
+// 4 -> 14.0, 5 -> 13.1, 6 -> 12.7, 7 -> 12.7 ms)
+#ifndef PTAP_MINB16
+#define PTAP_MINB16 6
+#endif
 #ifndef PTAP_MINB_Q4A
 #define PTAP_MINB_Q4A 4
 #endif
@@ -161,7 +166,7 @@ __device__ __forceinline__ void outer_scatter(const Ops &op, const MapArgs &mp, 
 }
 
 template <int G, int NAPCAP>
-__global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : 1) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
+__global__ void __launch_bounds__(256, G <= 8 ? PTAP_MINB : (G == 16 ? PTAP_MINB16 : 1)) k_outer_numeric_mapped(Ops op, const int32_t *rows, unsigned long long nrows,
                                                               MapArgs mp, OuterTargets tg, int do_send, int do_local,
                                                               int *status) {
   extern __shared__ __align__(16) unsigned char smem[];
