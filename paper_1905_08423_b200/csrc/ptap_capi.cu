@@ -117,6 +117,9 @@ struct ptap_plan {
   bool smap_interned = false;       // slot maps already interned (row-union path)
   bool rows_unstructured = false;   // sampled row structures do not repeat
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
+  std::vector<std::pair<int64_t, int64_t>> qa_runs;  // several ranks: runs of rows without A_o/P_o (q4a)
+  int32_t *qa_rest = nullptr;       // ... and the other bin-0 rows (q4)
+  int64_t qa_rest_n = 0;
   bool merged_deferred = false;     // merged plan without send rows: local structure built in symbolic_local
   double avg_p_row = 4.0;           // P entries per local fine row (arena sizing)
   bool want_maps = false;
@@ -808,6 +811,9 @@ ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
   pfree(p, p->maps.smap, st); pfree(p, p->maps.pmap, st);
   pfree(p, p->maps.nap, st); pfree(p, p->maps.po_srow, st);
   pfree(p, p->maps.poff, st); pfree(p, p->maps.cbase, st);
+  pfree(p, p->qa_rest, st);
+  p->qa_rest_n = 0;
+  p->qa_runs.clear();
   p->mapped = false;
   return PTAP_OK;
 }
@@ -920,12 +926,83 @@ ptap_status order_bins(ptap_plan *p, BinSet &bs, const Ops &op, cudaStream_t st)
   return PTAP_OK;
 }
 
+// Several ranks: the q4a kernel reads only A_d and P_d, so the local bin-0
+// rows whose A_o and P_o rows are empty -- the interior of a row block --
+// can run it; this finds their runs of consecutive rows (>= 256 rows, at
+// most 64 runs) and keeps the other bin-0 rows as a list for the q4 kernel.
+ptap_status build_q4a_runs(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  BinSet &bs = p->bins_local;
+  if (!p->mapped || !p->q4 || p->q4a || p->alg != PTAP_ALLATONCE || bs.count[0] == 0 ||
+      getenv("PTAP_NO_Q4A_RUNS") || p->c_nnz >= INT32_MAX)
+    return PTAP_OK;
+  const int64_t n = p->nloc, nb0 = bs.count[0];
+  uint8_t *flag = nullptr;
+  CKS(palloc(p, &flag, n, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(flag, 0, n > 0 ? n : 1, st));
+  const int32_t *b0 = bs.identity0 ? nullptr : bs.rows[0];  // identity bin: rows 0..n-1
+  CK(launch_pure_rows(nb0, b0, op, flag, st));
+  std::vector<uint8_t> hf(n);
+  std::vector<int32_t> rows(nb0);
+  CK(cudaMemcpyAsync(hf.data(), flag, n, cudaMemcpyDeviceToHost, st));
+  if (b0) CK(cudaMemcpyAsync(rows.data(), b0, nb0 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  else for (int64_t i = 0; i < nb0; ++i) rows[i] = (int32_t)i;
+  CK(cudaStreamSynchronize(st));
+  pfree(p, flag, st);
+  p->cnt.kernel_launches++;
+  std::vector<std::pair<int64_t, int64_t>> runs;
+  for (int64_t i = 0; i < n;) {
+    if (!hf[i]) { ++i; continue; }
+    int64_t j = i;
+    while (j < n && hf[j]) ++j;
+    if (j - i >= 256) runs.emplace_back(i, j - i);
+    i = j;
+  }
+  if (runs.empty() || runs.size() > 64) return PTAP_OK;
+  std::vector<uint8_t> in_run(n, 0);
+  for (auto &r : runs) std::fill(in_run.begin() + r.first, in_run.begin() + r.first + r.second, 1);
+  std::vector<int32_t> rest;
+  rest.reserve(nb0);
+  for (int32_t i : rows)
+    if (!in_run[i]) rest.push_back(i);
+  if (!rest.empty()) {
+    CKS(palloc(p, &p->qa_rest, (int64_t)rest.size(), CAT_PLAN, st));
+    CK(cudaMemcpyAsync(p->qa_rest, rest.data(), rest.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  p->qa_rest_n = (int64_t)rest.size();
+  if (!p->maps.cbase) {
+    CKS(palloc(p, &p->maps.cbase, ops->p_diag.nnz, CAT_PLAN, st));
+    CK(launch_build_cbase(ops->p_diag.nnz, op.pd_col, p->c_rp, p->maps.cbase, st));
+    p->cnt.kernel_launches++;
+  }
+  p->qa_runs = runs;
+  if (getenv("PTAP_TRACE")) {
+    int64_t in = 0;
+    for (auto &r : runs) in += r.second;
+    fprintf(stderr, "[ptap] q4a runs: %zu covering %lld rows, %lld bin-0 rows through q4\n", runs.size(), (long long)in,
+            (long long)p->qa_rest_n);
+  }
+  return PTAP_OK;
+}
+
 ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_send, int do_local, cudaStream_t st) {
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   if (p->mapped) {
     for (int q = 0; q < NBINS; ++q) {
       if (bs.count[q] == 0) continue;
       const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
+      if (q == 0 && !p->qa_runs.empty() && &bs == &p->bins_local && do_local && !do_send) {
+        for (auto &r : p->qa_runs) {
+          CK(launch_outer_numeric_q4a(op, (unsigned long long)r.second, p->maps, tg, p->d_status, st, (int)r.first));
+          p->cnt.kernel_launches++;
+        }
+        if (p->qa_rest_n > 0) {
+          CK(launch_outer_numeric_mapped(3, op, p->qa_rest, (unsigned long long)p->qa_rest_n, p->maps, tg, do_send,
+                                         do_local, p->d_status, st));
+          p->cnt.kernel_launches++;
+        }
+        continue;
+      }
       // q4a plans have no P_o (one-rank structure), so a merged pass's send
       // half is empty and its fused loop is the local loop
       if (q == 0 && p->q4a && bs.identity0 && do_local && (!do_send || op.po_rp == nullptr)) {
@@ -1224,6 +1301,7 @@ c_allocated:
   tr.mark(st, "merge slots / two-step bins");
   if (p->alg != PTAP_TWO_STEP) CKS(build_maps(p, op, ops, st));
   tr.mark(st, "position maps");
+  CKS(build_q4a_runs(p, op, ops, st));
   if (p->rows_unstructured && !(p->alg != PTAP_TWO_STEP && p->mapped) && !getenv("PTAP_NO_ROW_ORDER")) {
     // an operator whose rows do not repeat: visit rows in aggregate order
     // (k_row_order_keys) -- the hash numeric path, and two-step's C~ = A P

@@ -167,6 +167,7 @@ cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t
                           uint8_t *pool, int64_t *out, int pack_len, unsigned long long *claims, cudaStream_t st);
 // packed smap_rp entries of an interned plan: pool offset | map length << 40
 constexpr unsigned long long SMAP_OFF_MASK = (1ull << 40) - 1;
+cudaError_t launch_pure_rows(int64_t n, const int32_t *rows, const Ops &op, uint8_t *flag, cudaStream_t st);
 cudaError_t launch_build_poff(int64_t nnz, const int32_t *ad_col, const int64_t *pd_rp, int32_t *poff,
                               cudaStream_t st);
 cudaError_t launch_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t *c_rp, int32_t *cbase,

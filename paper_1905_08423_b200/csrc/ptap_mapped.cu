@@ -1166,6 +1166,29 @@ cudaError_t launch_intern(int pass, int64_t n, const uint8_t *src, const int64_t
   return cudaGetLastError();
 }
 
+// flag[i] = 1 for the listed rows that the q4a kernel can fold on its own:
+// an A_d row of at most 32 entries, no A_o entries, no P_o entries of its
+// own, and none in the P rows of its neighbours (q4a folds P_d rows only)
+__global__ void k_pure_rows(int64_t n, const int32_t *rows, Ops op, uint8_t *flag) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int32_t i = rows ? rows[q] : (int32_t)q;
+  const bool ao = op.ao_rp && op.ao_rp[i + 1] > op.ao_rp[i];
+  bool po = op.po_rp && op.po_rp[i + 1] > op.po_rp[i];
+  const int64_t t0 = op.ad_rp[i], t1 = op.ad_rp[i + 1];
+  if (op.po_rp && !po)
+    for (int64_t t = t0; t < t1; ++t) {
+      const int32_t k = op.ad_col[t];
+      if (op.po_rp[k + 1] > op.po_rp[k]) { po = true; break; }
+    }
+  flag[i] = (!ao && !po && t1 - t0 <= 32) ? 1 : 0;
+}
+
+cudaError_t launch_pure_rows(int64_t n, const int32_t *rows, const Ops &op, uint8_t *flag, cudaStream_t st) {
+  if (n > 0) k_pure_rows<<<nb(n, 256), 256, 0, st>>>(n, rows, op, flag);
+  return cudaGetLastError();
+}
+
 // poff[e] = P_rp[k] | (P_rp[k+1] - P_rp[k]) << 28 for A entry e with column k
 // (the plan checks nnz(P_d) < 2^28 and P rows <= 15): the q4a fold reads this
 // instead of A's column and P's row bounds, one dependent load less per chunk
