@@ -15,6 +15,7 @@
 //   k_ptc_numeric<G>      two-step P^T C~ values (staging or C)              _kernels.py:583-677
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ptap_device.cuh"
@@ -1360,6 +1361,16 @@ cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int
   const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
   unsigned char *gtables = s.gtables;
   cudaError_t e;
+  static const bool g16 = !getenv("PTAP_NO_SYM16");
+  if (g16 && s.bin == 1 && !gtables) {
+    // AP rows of 33..128 keys (config 4): 16 lanes per row, two rows per warp
+    const int gpc = warps * 2;
+    const size_t sm = group_bytes(log2t, false, 16) * gpc;
+    if ((e = set_smem(k_outer_symbolic<16, false>, sm)) != cudaSuccess) return e;
+    k_outer_symbolic<16, false><<<grid_for(nrows, gpc, max_ctas), warps * 32, sm, stream>>>(
+        op, rows, nrows, log2t, gtables, do_send, do_local, local, send, mo, status);
+    return cudaGetLastError();
+  }
   PTAP_ROWKERNEL_DISPATCH(k_outer_symbolic, false, op, rows, nrows, log2t, gtables, do_send, do_local, local, send,
                           mo, status);
 }
