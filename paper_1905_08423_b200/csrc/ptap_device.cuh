@@ -104,7 +104,14 @@ __device__ __forceinline__ int table_find(const int32_t *keys, int log2t, int32_
 
 // Pairs (A entry, P entry) of one batch of A entries, flattened in the
 // reference's fold order and staged in shared memory per lane group.
-constexpr int PAIRS_PER_LANE = 8;  // window = PAIRS_PER_LANE * GROUP pairs
+// The hash-table row kernels broadcast each A entry by shuffle and never read
+// this window, so it is sized 0: its 12 bytes per pair per group only cost
+// resident warps (config 5 hash numeric at 2 M points: 8 -> 6.40 ms,
+// 0 -> 4.48 ms).
+#ifndef PTAP_PAIRS_PER_LANE
+#define PTAP_PAIRS_PER_LANE 0
+#endif
+constexpr int PAIRS_PER_LANE = PTAP_PAIRS_PER_LANE;  // window = PAIRS_PER_LANE * GROUP pairs
 
 struct PStage {
   int32_t *desc;  // [window] P entry index; bit 31 set = P_o entry
