@@ -1206,9 +1206,11 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
                                                  int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
                                                  const int64_t *pd_rp, const int32_t *pd_col,
                                                  const int64_t *pmap_rp, uint8_t *pmap, int *status) {
+  // compacted keys need only CU_MAX entries (a longer union fails the row
+  // anyway): 38 KB per CTA instead of 44, one more resident CTA per SM
   __shared__ int32_t keys_all[8][CU_T];
-  __shared__ int32_t lk_all[8][CU_T];
-  __shared__ uint16_t lpos_all[8][CU_T];
+  __shared__ int32_t lk_all[8][CU_MAX];
+  __shared__ uint16_t lpos_all[8][CU_MAX];
   __shared__ uint8_t rank_all[8][CU_T];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   int32_t *keys = keys_all[warp], *lk = lk_all[warp];
@@ -1240,8 +1242,10 @@ __global__ void __launch_bounds__(256) k_c_union(int64_t ncl, const int64_t *t_r
       const unsigned b = __ballot_sync(FULL, k != EMPTY32);
       if (k != EMPTY32) {
         const int at = n + __popc(b & ((1u << lane) - 1u));
-        lk[at] = k;
-        lpos[at] = (uint16_t)(s0 + lane);
+        if (at < CU_MAX) {
+          lk[at] = k;
+          lpos[at] = (uint16_t)(s0 + lane);
+        }
       }
       n += __popc(b);
     }
