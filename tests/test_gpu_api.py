@@ -12,6 +12,11 @@ from tests.conftest import csr_from_arrays, load_golden, row_scaled_err, run_pta
 
 pytestmark = pytest.mark.gpu
 
+# Two all-at-once passes sum each C entry's ~13 contributions in whatever order
+# the fp64 reductions land, so repeated or rearranged passes agree to a few
+# ulps of the row's largest entry, not bitwise (measured up to 1.1e-15).
+RUN_TOL = 1e-14
+
 
 def _cfg3(n=16):
     return gen.config_operands(gen.CONFIGS["cfg3"], n_fine=n)
@@ -20,7 +25,7 @@ def _cfg3(n=16):
 def test_repeated_numeric_protocol_one_symbolic_eleven_numeric():
     """1 symbolic + 11 numeric: counters, and the two-step passes
     are bitwise identical (deterministic ordered folds); all-at-once passes
-    agree to a row-scaled 1e-15 (atomics order varies)."""
+    agree to a row-scaled RUN_TOL (atomics order varies)."""
     A, P = _cfg3()
     ctx = pk.single_rank_context()
     a, p = pk.distribute(A, P, 1, 0)
@@ -33,7 +38,7 @@ def test_repeated_numeric_protocol_one_symbolic_eleven_numeric():
             if alg == "two-step":
                 assert np.array_equal(o.view(np.uint64), outs[0].view(np.uint64))
             else:
-                assert row_scaled_err(ip, o, outs[0]) <= 1e-15
+                assert row_scaled_err(ip, o, outs[0]) <= RUN_TOL
 
 
 def test_values_change_structure_fixed_linearity():
@@ -49,7 +54,7 @@ def test_values_change_structure_fixed_linearity():
         c4 = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
         a.local.diag.values /= 4.0
         ip = plan.c_alloc.local.diag.row_offsets
-        assert row_scaled_err(ip, c4, 4.0 * c0) <= 1e-15
+        assert row_scaled_err(ip, c4, 4.0 * c0) <= RUN_TOL
 
 
 def test_cache_free_releases_plan_keeps_c():
@@ -103,7 +108,7 @@ def test_memory_two_step_vs_all_at_once():
 
 def test_mapped_and_hash_numeric_paths_agree():
     """The plan-mapped numeric pass (default) and the hash pass
-    (PTAP_NO_MAPS=1) give the same C (row-scaled 1e-15)."""
+    (PTAP_NO_MAPS=1) give the same C (row-scaled RUN_TOL)."""
     A, P = _cfg3(20)
     c_map, _ = run_ptap(A, P, 1, "allatonce")
     os.environ["PTAP_NO_MAPS"] = "1"
@@ -112,7 +117,7 @@ def test_mapped_and_hash_numeric_paths_agree():
     finally:
         del os.environ["PTAP_NO_MAPS"]
     assert c_map.structure_equal(c_hash)
-    assert row_scaled_err(c_map.row_offsets, c_map.values, c_hash.values) <= 1e-15
+    assert row_scaled_err(c_map.row_offsets, c_map.values, c_hash.values) <= RUN_TOL
 
 
 def test_interned_maps_shrink_plan_and_match_private_maps():
@@ -136,7 +141,7 @@ def test_interned_maps_shrink_plan_and_match_private_maps():
     finally:
         del os.environ["PTAP_NO_INTERN"]
     assert np.array_equal(ip, ip2) and np.array_equal(j, j2)
-    assert row_scaled_err(ip, v, v2) <= 1e-15
+    assert row_scaled_err(ip, v, v2) <= RUN_TOL
     assert shared < 0.5 * private, (shared, private)
 
 
@@ -203,7 +208,7 @@ def test_standalone_spgemm_matches_reference_golden():
 def test_streamed_host_numeric_matches_one_shot():
     """At one rank the all-at-once pass with host operands streams A's values
     up in row blocks and final C rows back; the result equals the one-shot
-    path (same kernels) within the atomics' row-scaled 1e-15, for several
+    path (same kernels) within the atomics' row-scaled RUN_TOL, for several
     block counts, and numeric_runs counts passes, not blocks."""
     A, P = _cfg3(20)
     ctx = pk.single_rank_context()
@@ -221,7 +226,7 @@ def test_streamed_host_numeric_matches_one_shot():
             got = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
         finally:
             del os.environ["PTAP_UPLOAD_BLOCKS"]
-        assert row_scaled_err(ip, got, ref) <= 1e-15
+        assert row_scaled_err(ip, got, ref) <= RUN_TOL
     assert plan.counters.numeric_runs == 4
 
 
@@ -238,5 +243,5 @@ def test_streamed_path_falls_back_when_rows_not_range_addressable():
     assert getattr(plan, "_stream_ok", True) is False
     c2 = pk.run_numeric(a, p, plan, ctx).diag.values.copy()
     ip = plan.c_alloc.local.diag.row_offsets
-    assert row_scaled_err(ip, c2, c1) <= 1e-15
+    assert row_scaled_err(ip, c2, c1) <= RUN_TOL
     assert plan.counters.numeric_runs == 2
