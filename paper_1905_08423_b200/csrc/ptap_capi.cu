@@ -339,7 +339,10 @@ ptap_status arena_alloc(ptap_plan *p, Arena &ar, unsigned long long min_keys, cu
   ar.mask = cap - 1;
   ar.m = (unsigned long long)p->m;
   ar.log2b = 0;
-  if (bucket_rows > 0 && !getenv("PTAP_HASHED_ARENA")) {
+  // row buckets suit operators whose rows repeat; on an unstructured one
+  // (config 5) bucket runs overflow and chain (4 M points: 535 vs 20 ms), so
+  // its arena is hashed
+  if (bucket_rows > 0 && !getenv("PTAP_HASHED_ARENA") && !p->rows_unstructured) {
     unsigned long long r = 1;
     while (r < bucket_rows) r <<= 1;
     int lb = 0;
