@@ -490,7 +490,14 @@ template <typename K>
 static unsigned long long grid_cap(K kern, int threads, size_t smem) {
   static int mode = -1;
   if (mode < 0) mode = getenv("PTAP_GRID_RESIDENT") ? 1 : 0;
-  if (!mode) return 148ull * 64;
+  if (!mode) {
+    // CTAs per SM in the grid (PTAP_GRID_MULT): enough that each CTA folds
+    // one or two row chunks, so the rows in flight advance as one band in
+    // launch order (cfg3 L1: 64 -> 7.16 ms, 256 -> 7.09, 1024 -> 6.92,
+    // 2048 -> 6.95; cfg4 12.70 -> 12.35 ms)
+    static const int mult = getenv("PTAP_GRID_MULT") ? atoi(getenv("PTAP_GRID_MULT")) : 1024;
+    return 148ull * (unsigned long long)(mult > 0 ? mult : 1024);
+  }
   int dev = 0, nsm = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
