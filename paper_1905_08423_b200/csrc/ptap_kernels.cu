@@ -931,9 +931,12 @@ __global__ void k_arena_rehash(Arena from, Arena to, int *status) {
 // row's pattern is ranked -- no second walk and no per-pair probe.  The map
 // bytes are assembled in shared memory and stored as aligned 32-bit words.
 constexpr int SQ_R = 8, SQ_G = 4, SQ_LOG2T = 6, SQ_T = 64, SQ_SMB = 132;
-struct SqWarp {
-  int32_t keys[SQ_R][SQ_T];
-  int32_t lk[SQ_R][SQ_T];       // compacted keys
+// keys/lk rows padded to 68 words: the 8 row groups of a warp read the same
+// index of their own rows at once, and a 64-word stride put all 8 in one bank
+constexpr int SQ_TP = SQ_T + 4;
+struct __align__(16) SqWarp {
+  int32_t keys[SQ_R][SQ_TP];
+  int32_t lk[SQ_R][SQ_TP];      // compacted keys, INT32_MAX-padded to a multiple of 4
   uint8_t lpos[SQ_R][SQ_T];     // their table positions
   uint8_t slot_of[SQ_R][SQ_T];  // table position -> slot (rank)
   uint32_t sm[SQ_R][SQ_SMB / 4];  // slot bytes of the row, at (start & 3) + pair
@@ -1063,18 +1066,38 @@ __global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t
       }
       n += __popc(b);
     }
+    if (gl < 4) W.lk[r][n + gl] = INT32_MAX;  // n <= SQ_T: the pad fits the row
     __syncwarp();
-    // slot = rank of the key in the row (sorted pattern), no sort needed
-    if (i >= 0) {
-      int32_t *pat = mo.pat + mo.pat_rp[i];
-      for (int x = gl; x < n; x += G) {
-        const int32_t g = W.lk[r][x];
-        int rk = 0;
-        for (int y = 0; y < n; ++y) rk += W.lk[r][y] < g;
-        pat[rk] = g;
-        W.slot_of[r][W.lpos[r][x]] = (uint8_t)rk;
+    // slot = rank of the key in the row (sorted pattern), no sort needed: the
+    // lane's keys stay in registers and the row streams past them 4 at a time
+    {
+      constexpr int KPL = SQ_T / G;
+      const int nmax = __reduce_max_sync(FULL, i >= 0 ? n : 0);
+      int32_t mine[KPL];
+      int rk[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+        mine[q] = gl + G * q < n ? W.lk[r][gl + G * q] : INT32_MAX;
+        rk[q] = 0;
       }
-      if (gl == 0) mo.nap[i] = (uint8_t)n;
+      for (int y0 = 0; y0 < n; y0 += 4) {
+        const int4 v = *reinterpret_cast<const int4 *>(&W.lk[r][y0]);
+#pragma unroll
+        for (int q = 0; q < KPL; ++q)
+          if (G * q < nmax) rk[q] += (v.x < mine[q]) + (v.y < mine[q]) + (v.z < mine[q]) + (v.w < mine[q]);
+      }
+      if (i >= 0) {
+        int32_t *pat = mo.pat + mo.pat_rp[i];
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) {
+          const int x = gl + G * q;
+          if (x < n) {
+            pat[rk[q]] = mine[q];
+            W.slot_of[r][W.lpos[r][x]] = (uint8_t)rk[q];
+          }
+        }
+        if (gl == 0) mo.nap[i] = (uint8_t)n;
+      }
     }
     __syncwarp();
     // slot bytes: table position -> slot, keeping the first-product bit; then
