@@ -141,7 +141,7 @@ typedef struct {
     int64_t nnz_staging;
     int64_t mac_ap;                    /* multiply-adds of the A*P rows       */
     int64_t mac_outer;                 /* multiply-adds of the outer products */
-    int64_t numeric_path;              /* all-at-once/merged numeric: 1 plan maps, 0 hash tables */
+    int64_t numeric_path;              /* all-at-once/merged numeric: 2 deterministic owner-computes, 1 plan maps, 0 hash tables */
     int64_t map_bytes;                 /* plan maps kept (slot + position pools, interned) */
     int64_t row_structures_ppm;        /* distinct row structures per 1e6 sampled rows, -1: not sampled */
 } ptap_counters;
@@ -153,6 +153,13 @@ const char *ptap_version(void);
 
 ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan **out);
 ptap_status ptap_plan_destroy(ptap_plan *plan);
+/* Plan options, set between create and the symbolic calls.
+ *   "deterministic" (0/1): numeric passes bitwise repeatable and, at one rank,
+ *     bit-identical to the reference's summation order (src/tripleproduct.py:12-16,
+ *     src/_kernels.py:446-515): the owner-computes kernel of ptap_tile.cu
+ *     replaces the fp64-atomic scatter when the plan's local loop has
+ *     one-rank structure (counters.numeric_path == 2 when it is in use). */
+ptap_status ptap_plan_set_option(ptap_plan *plan, const char *key, int64_t value);
 
 /* Symbolic, phase 1: AP-row binning and the send-side structure C_s (all
  * variants), plus (two-step) C~ and the local transposes. */

@@ -117,6 +117,11 @@ struct ptap_plan {
   bool smap_interned = false;       // slot maps already interned (row-union path)
   bool rows_unstructured = false;   // sampled row structures do not repeat
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
+  bool tile = false;                // ... and the deterministic owner-computes kernel replaces it
+  bool deterministic = false;       // plan option: bitwise-repeatable numeric passes (tile kernel)
+  TileArgs ta{};
+  int64_t max_nap = 0;              // widest AP row
+  int64_t qmap_bytes = 0;           // tile gather maps (interned)
   std::vector<std::pair<int64_t, int64_t>> qa_runs;  // several ranks: runs of rows without A_o/P_o (q4a)
   int32_t *qa_rest = nullptr;       // ... and the other bin-0 rows (q4)
   int64_t qa_rest_n = 0;
@@ -592,6 +597,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   CK(cudaStreamSynchronize(st));
   p->cnt.kernel_launches += 3;
   tr.mark(st, "  maps: maxima");
+  p->max_nap = (int64_t)h[0];
   if (h[0] > 255 || h[1] > 65535 || h[2] > 255) return PTAP_OK;  // hash path for this plan
   // maps pay for themselves when rows repeat (interned, a small pool); on an
   // operator whose rows do not repeat they would cost about as much memory as
@@ -767,6 +773,188 @@ ptap_status intern_map(ptap_plan *p, uint8_t *&src, int64_t *&src_rp, int64_t n,
   return PTAP_OK;
 }
 
+// ---- deterministic owner-computes numeric plan (ptap_tile.cu) ----------------
+void free_tile(ptap_plan *p, cudaStream_t st) {
+  TileArgs &t = p->ta;
+  pfree(p, t.ap_off, st); pfree(p, t.ring, st); pfree(p, t.own_rp, st); pfree(p, t.t_pidx, st);
+  pfree(p, t.t_rp, st); pfree(p, t.t_row, st); pfree(p, t.t_jx, st); pfree(p, t.rd_rp, st);
+  pfree(p, t.rd_blk, st); pfree(p, t.expect, st); pfree(p, t.flags, st); pfree(p, t.readcnt, st);
+  pfree(p, t.ctl, st);
+  pfree(p, t.qmap, st); pfree(p, t.qmap_rp, st); pfree(p, t.pr_n, st); pfree(p, t.pr_k, st);
+  pfree(p, t.t_jx, st);
+  t = TileArgs{};
+  p->tile = false;
+}
+
+// Eligible: one-rank structure (the q4a plan: no A_o / P_o, A rows <= 32),
+// interned maps, AP rows <= 32 slots, C rows <= 64 entries with <= 32
+// contributors, and a contributor span that keeps the AP ring small.
+ptap_status build_tile(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  p->tile = false;
+  if (!(p->deterministic || getenv("PTAP_DETERMINISTIC")) || getenv("PTAP_NO_TILE")) return PTAP_OK;
+  if (!p->mapped || !p->q4a || p->alg == PTAP_TWO_STEP || p->max_nap > 32) return PTAP_OK;
+  const int64_t n = p->nloc, ncl = p->ncl, pnnz = ops->p_diag.nnz;
+  if (n <= 0 || ncl <= 0 || pnnz >= INT32_MAX || ops->a_diag.nnz >= INT32_MAX || n >= INT32_MAX - 2 * TILE_ROWS)
+    return PTAP_OK;
+  unsigned long long *stats = nullptr;  // span, max contributors, largest block, largest owner, A per block,
+  CKS(palloc(p, &stats, 8, CAT_TRANSIENT, st));  // staged P values, staged blocks
+  CK(cudaMemsetAsync(stats, 0, 8 * sizeof(unsigned long long), st));
+  unsigned long long *cmax_d = p->d_u64 + 12;
+  CK(cudaMemsetAsync(cmax_d, 0, sizeof(unsigned long long), st));
+  CK(launch_max_rowlen(ncl, p->c_rp, cmax_d, st));
+  TileArgs &t = p->ta;
+  t = TileArgs{};
+  const int nblk = (int)((n + TILE_ROWS - 1) / TILE_ROWS);
+  t.nloc = (int32_t)n;
+  t.nblk = nblk;
+  t.napc = (int32_t)std::max<int64_t>(1, p->max_nap);
+  // per-block AP offsets, the largest block, and the P rows each block stages
+  uint16_t *ap_off = nullptr;
+  uint8_t *pr_n = nullptr;
+  int2 *pr_k = nullptr;
+  CKS(palloc(p, &ap_off, n, CAT_PLAN, st));
+  CKS(palloc(p, &pr_n, nblk, CAT_PLAN, st));
+  CKS(palloc(p, &pr_k, (int64_t)nblk * TILE_MAXRUN, CAT_PLAN, st));
+  t.ap_off = ap_off; t.pr_n = pr_n; t.pr_k = pr_k;
+  CK(launch_tile_apoff(n, op.ad_rp, op.pd_rp, p->maps.nap, ap_off, stats, st));
+  // P runs staged in shared memory: measured slower (17.4 vs 13.9 ms on
+  // config 3: the extra shared memory costs resident CTAs), so opt-in
+  const bool pstage = getenv("PTAP_TILE_PSTAGE") != nullptr;
+  const int pvcap = pstage ? 3072 : 0;
+  t.pstage = pstage ? 1 : 0;
+  if (pstage)
+    CK(launch_tile_pruns(nblk, n, op.ad_rp, op.ad_col, op.pd_rp, pnnz, pvcap, 1024, pr_n, pr_k, stats, st));
+  else
+    CK(cudaMemsetAsync(pr_n, 0, nblk, st));
+  unsigned long long hs[8], cmax = 0;
+  CK(cudaMemcpyAsync(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&cmax, cmax_d, sizeof(cmax), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (cmax > (unsigned long long)TILE_MAX_CROW || hs[4] > 64 * 32) {
+    pfree(p, stats, st);
+    free_tile(p, st);
+    return PTAP_OK;
+  }
+  const int64_t blkcap = std::max<int64_t>(2, (int64_t)hs[2]);
+  tile_smem_layout(t, (int)hs[4], pstage ? (int)hs[5] : 0, pstage ? (int)hs[7] : 0);
+  const int grid = tile_grid(t);
+  // ownership delay: C row J is gathered at least `delay` items after the
+  // block of its last contributor, so its contributors were published a
+  // full grid of items earlier and the gather practically never waits
+  const int delay = getenv("PTAP_TILE_DELAY") ? atoi(getenv("PTAP_TILE_DELAY")) : grid;
+  const int64_t wide = std::max<int64_t>(ncl, nblk + delay + 2);
+  const size_t sbytes = std::max(tile_scan_scratch(wide), tile_owner_scratch(ncl));
+  uint8_t *scratch = nullptr;
+  int32_t *cnt = nullptr, *cursor = nullptr, *owner = nullptr;
+  long long *key = nullptr;
+  CKS(palloc(p, &scratch, (int64_t)sbytes, CAT_TRANSIENT, st));
+  CKS(palloc(p, &cnt, wide + 1, CAT_TRANSIENT, st));
+  CKS(palloc(p, &cursor, wide + 1, CAT_TRANSIENT, st));
+  int32_t *t_rp = nullptr, *t_row = nullptr, *t_pidx = nullptr, *own_rp = nullptr;
+  uint8_t *t_jx = nullptr;
+  CKS(palloc(p, &t_rp, ncl + 1, CAT_PLAN, st));
+  CKS(palloc(p, &t_row, pnnz, CAT_PLAN, st));
+  CKS(palloc(p, &t_pidx, pnnz, CAT_PLAN, st));
+  CKS(palloc(p, &t_jx, pnnz, CAT_TRANSIENT, st));
+  t.t_rp = t_rp; t.t_row = t_row; t.t_pidx = t_pidx; t.t_jx = t_jx;
+  CK(launch_tile_transpose(n, ncl, op.pd_rp, op.pd_col, pnnz, cnt, t_rp, cursor, t_row, t_jx, scratch, sbytes,
+                           p->d_status, st));
+  CKS(palloc(p, &owner, ncl, CAT_TRANSIENT, st));
+  CKS(palloc(p, &key, ncl, CAT_TRANSIENT, st));
+  CK(launch_tile_owners(ncl, nblk, delay, op.pd_rp, t_rp, t_row, t_jx, t_pidx, key, owner, stats, scratch, sbytes,
+                        st));
+  pfree(p, key, st);
+  CK(cudaMemcpyAsync(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->cnt.kernel_launches += 10;
+  const int64_t span = (int64_t)hs[0], kmax = (int64_t)hs[1];
+  const int nitems = std::max<int>(nblk, (int)hs[3] + 1);
+  t.nitems = nitems;
+  const int64_t R = std::min<int64_t>(nblk, span + 2 * (int64_t)grid + 64);
+  if (kmax > 32 || span > 32768 || R * blkcap >= INT32_MAX || R * blkcap * 8 > (int64_t(512) << 20)) {
+    pfree(p, scratch, st); pfree(p, cnt, st); pfree(p, cursor, st); pfree(p, owner, st); pfree(p, stats, st);
+    free_tile(p, st);
+    return PTAP_OK;
+  }
+  const unsigned long long staged_blocks = hs[6];
+  pfree(p, stats, st);
+  CKS(palloc(p, &own_rp, nitems + 1, CAT_PLAN, st));
+  t.own_rp = own_rp;
+  CK(launch_tile_own_rp(nitems, ncl, owner, own_rp, st));
+  pfree(p, owner, st);
+  // reader lists
+  int32_t *rd_rp = nullptr, *rd_blk = nullptr;
+  uint32_t *expect = nullptr;
+  CKS(palloc(p, &rd_rp, nitems + 1, CAT_PLAN, st));
+  CKS(palloc(p, &expect, nblk, CAT_PLAN, st));
+  t.rd_rp = rd_rp; t.expect = expect;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nitems + 1), st));
+  CK(cudaMemsetAsync(expect, 0, sizeof(uint32_t) * nblk, st));
+  CK(launch_tile_reads(0, nitems, 0, (int)span, own_rp, t_rp, t_row, cnt, nullptr, nullptr, nullptr, st));
+  CK(launch_tile_scan32(cnt, rd_rp, nitems, scratch, sbytes, st));
+  int32_t nrd = 0;
+  CK(cudaMemcpyAsync(&nrd, rd_rp + nitems, sizeof(nrd), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CKS(palloc(p, &rd_blk, nrd, CAT_PLAN, st));
+  t.rd_blk = rd_blk;
+  CK(launch_tile_reads(1, nitems, 0, (int)span, own_rp, t_rp, t_row, nullptr, rd_rp, rd_blk, expect, st));
+  pfree(p, scratch, st); pfree(p, cnt, st); pfree(p, cursor, st);
+  // gather maps (inverse position maps per C row), interned like the others
+  {
+    int64_t *qlen = nullptr, *qrp = nullptr, *sc = nullptr;
+    uint8_t *qm = nullptr;
+    CKS(palloc(p, &qlen, ncl, CAT_TRANSIENT, st));
+    CKS(palloc(p, &qrp, ncl + 1, CAT_PLAN, st));
+    CKS(palloc(p, &sc, scan_scratch_elems(ncl), CAT_TRANSIENT, st));
+    CK(launch_tile_qmap(ncl, t, p->c_rp, qlen, nullptr, nullptr, nullptr, nullptr, nullptr, 0, st));
+    CK(scan_exclusive(qlen, qrp, ncl, sc, st));
+    int64_t qtot = 0;
+    CK(cudaMemcpyAsync(&qtot, qrp + ncl, sizeof(qtot), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pfree(p, qlen, st);
+    pfree(p, sc, st);
+    CKS(palloc(p, &qm, qtot + 16, CAT_PLAN, st));
+    CK(launch_tile_qmap(ncl, t, p->c_rp, nullptr, qrp, p->maps.nap, p->maps.pmap_rp, p->maps.pmap, qm, 1, st));
+    int64_t pool = 0;
+    CKS(intern_map(p, qm, qrp, ncl, qtot, false, &pool, st));
+    pfree(p, t_jx, st);
+    t.t_jx = nullptr;
+    t.qmap = qm;
+    t.qmap_rp = qrp;
+    p->qmap_bytes = pool;
+    p->cnt.kernel_launches += 2;
+  }
+  uint32_t *flags = nullptr, *readcnt = nullptr, *ctl = nullptr;
+  CKS(palloc(p, &flags, nblk, CAT_PLAN, st));
+  CKS(palloc(p, &readcnt, nblk, CAT_PLAN, st));
+  CKS(palloc(p, &ctl, 4, CAT_PLAN, st));
+  CK(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * nblk, st));
+  CK(cudaMemsetAsync(readcnt, 0, sizeof(uint32_t) * nblk, st));
+  CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * 4, st));
+  t.flags = flags; t.readcnt = readcnt; t.ctl = ctl;
+  double *ring = nullptr;
+  CKS(palloc(p, &ring, R * blkcap, CAT_PLAN, st));
+  t.ring = ring;
+  t.ring_blocks = (int32_t)R;
+  t.blkcap = (int32_t)blkcap;
+  t.grid = grid;
+  t.dbg = getenv("PTAP_TILE_DBG") ? atoi(getenv("PTAP_TILE_DBG")) : 0;
+  p->cnt.kernel_launches += 3;
+  int s = 0;
+  CKS(read_status(p, st, &s));
+  if (s) {
+    free_tile(p, st);
+    return status_to_error(s, "tile plan");
+  }
+  p->tile = true;
+  if (getenv("PTAP_TRACE"))
+    fprintf(stderr,
+            "[ptap] tile plan: %d blocks (%llu stage P), %d items (delay %d), span %lld, ring %lld x %lld doubles, "
+            "grid %d, smem %d B, %d reads, gather maps %lld B\n",
+            nblk, staged_blocks, nitems, delay, (long long)span, (long long)R, (long long)blkcap, grid, t.sm_total, nrd, (long long)p->qmap_bytes);
+  return PTAP_OK;
+}
+
 // Part 2 (C and the staging allocated): position maps (unless the row-union
 // pass already wrote them), then drop the transient patterns.  Falls back to
 // the hash path if a target row is wider than a byte can address.
@@ -783,12 +971,6 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     }
   }
   p->mapped = ok;
-  // C row start per P_d entry for the q4a outer phase (4 B per P entry)
-  if (ok && p->q4a && p->c_nnz < INT32_MAX && !getenv("PTAP_NO_CBASE")) {
-    CKS(palloc(p, &p->maps.cbase, ops->p_diag.nnz, CAT_PLAN, st));
-    CK(launch_build_cbase(ops->p_diag.nnz, op.pd_col, p->c_rp, p->maps.cbase, st));
-    p->cnt.kernel_launches++;
-  }
   pfree(p, p->pat, st);
   pfree(p, p->pat_rp, st);
   p->mo = MapOut{};
@@ -799,6 +981,14 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     CKS(intern_map(p, p->maps.pmap, p->maps.pmap_rp, p->nloc, p->pmap_bytes, false, &p->pmap_bytes, st));
     p->cnt.numeric_path = 1;
     p->cnt.map_bytes = p->smap_bytes + p->pmap_bytes;
+    CKS(build_tile(p, op, ops, st));
+    if (p->tile) p->cnt.numeric_path = 2;
+  }
+  // C row start per P_d entry for the q4a outer phase (4 B per P entry)
+  if (ok && p->q4a && !p->tile && p->c_nnz < INT32_MAX && !getenv("PTAP_NO_CBASE")) {
+    CKS(palloc(p, &p->maps.cbase, ops->p_diag.nnz, CAT_PLAN, st));
+    CK(launch_build_cbase(ops->p_diag.nnz, op.pd_col, p->c_rp, p->maps.cbase, st));
+    p->cnt.kernel_launches++;
   }
   if (!ok) {
     pfree(p, p->maps.smap_rp, st);
@@ -810,6 +1000,7 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
 }
 
 ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
+  free_tile(p, st);
   pfree(p, p->maps.smap_rp, st); pfree(p, p->maps.pmap_rp, st);
   pfree(p, p->maps.smap, st); pfree(p, p->maps.pmap, st);
   pfree(p, p->maps.nap, st); pfree(p, p->maps.po_srow, st);
@@ -1009,6 +1200,11 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
       // q4a plans have no P_o (one-rank structure), so a merged pass's send
       // half is empty and its fused loop is the local loop
       if (q == 0 && p->q4a && bs.identity0 && do_local && (!do_send || op.po_rp == nullptr)) {
+        if (p->tile) {  // deterministic owner-computes pass: writes every C entry once
+          CK(launch_tile_numeric(op, p->maps, p->ta, p->c_rp, p->c_val, 0, p->ta.nblk, true, st));
+          p->cnt.kernel_launches += 2;
+          continue;
+        }
         CK(launch_outer_numeric_q4a(op, (unsigned long long)bs.count[q], p->maps, tg, p->d_status, st, 0));
         p->cnt.kernel_launches++;
         continue;
@@ -1082,6 +1278,15 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
   }
   *out = p;
   return PTAP_OK;
+}
+
+ptap_status ptap_plan_set_option(ptap_plan *p, const char *key, int64_t value) {
+  if (!p || !key) return fail(PTAP_ERR_VALUE, "null argument");
+  if (!strcmp(key, "deterministic")) {
+    p->deterministic = value != 0;
+    return PTAP_OK;
+  }
+  return fail(PTAP_ERR_VALUE, std::string("unknown plan option '") + key + "'");
 }
 
 ptap_status ptap_plan_destroy(ptap_plan *p) {
@@ -1328,6 +1533,11 @@ c_allocated:
   return PTAP_OK;
 }
 
+// the tile pass is the whole local loop and stores every C entry: no zero fill
+static bool tile_writes_all(const ptap_plan *p, const BinSet &bs, const Ops &op) {
+  return p->tile && p->q4a && bs.identity0 && op.po_rp == nullptr && p->r_nnz == 0;
+}
+
 static ptap_status numeric_ready(ptap_plan *p) {
   if (!p) return fail(PTAP_ERR_VALUE, "null plan");
   if (p->released) return fail(PTAP_ERR_DRIFT, "plan internals were released (free-after-solve); rebuild the plan");
@@ -1356,8 +1566,9 @@ ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stre
   }
   bool merged = p->alg == PTAP_MERGED;
   if (p->s_nnz > 0) CK(cudaMemsetAsync(p->s_val, 0, sizeof(double) * p->s_nnz, st));
-  if (merged && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   BinSet &bs = merged ? p->bins_all : p->bins_send;
+  if (merged && p->c_nnz > 0 && !tile_writes_all(p, bs, op))
+    CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   CKS(run_outer_numeric(p, op, bs, 1, merged ? 1 : 0, st));
   p->cnt.numeric_row_kernel_calls += bs.selected;
   return PTAP_OK;
@@ -1376,7 +1587,8 @@ ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *str
     }));
     p->cnt.numeric_row_kernel_calls += p->nloc;
   } else if (p->alg == PTAP_ALLATONCE) {
-    if (p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
+    if (p->c_nnz > 0 && !tile_writes_all(p, p->bins_local, op))
+      CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
     CKS(run_outer_numeric(p, op, p->bins_local, 0, 1, st));
     p->cnt.numeric_row_kernel_calls += p->bins_local.selected;
   }
@@ -1393,6 +1605,18 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
   if (row_lo < 0 || row_hi > p->nloc || row_lo > row_hi) return fail(PTAP_ERR_VALUE, "row range");
   cudaStream_t st = (cudaStream_t)stream;
   Ops op = make_ops(ops);
+  if (p->tile) {
+    // block-aligned ranges (the last may end at nloc); the first call of a
+    // pass opens a new epoch
+    if (row_lo % TILE_ROWS || (row_hi % TILE_ROWS && row_hi != p->nloc))
+      return fail(PTAP_ERR_VALUE, "row range must be aligned to the plan's 64-row blocks");
+    const int b0 = (int)(row_lo / TILE_ROWS), b1 = (int)((row_hi + TILE_ROWS - 1) / TILE_ROWS);
+    CK(launch_tile_numeric(op, p->maps, p->ta, p->c_rp, p->c_val, b0, b1, (flags & 1) != 0, st));
+    p->cnt.kernel_launches += 2;
+    p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
+    if (flags & 2) p->cnt.numeric_runs++;
+    return PTAP_OK;
+  }
   if ((flags & 1) && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
   if (row_hi > row_lo) {
@@ -1413,7 +1637,8 @@ ptap_status ptap_plan_c_last_row(ptap_plan *p, const ptap_operands *ops, int32_t
   CKS(numeric_ready(p));
   CKS(validate(ops));
   if (!last && p->ncl > 0) return fail(PTAP_ERR_VALUE, "null output");
-  CK(launch_c_last_row(p->nloc, ops->p_diag.row_ptr, ops->p_diag.col, p->ncl, last, (cudaStream_t)stream));
+  if (p->tile) CK(launch_tile_c_last(p->ncl, p->ta, last, (cudaStream_t)stream));
+  else CK(launch_c_last_row(p->nloc, ops->p_diag.row_ptr, ops->p_diag.col, p->ncl, last, (cudaStream_t)stream));
   return PTAP_OK;
 }
 

@@ -175,4 +175,62 @@ cudaError_t launch_build_cbase(int64_t nnz, const int32_t *pd_col, const int64_t
 cudaError_t launch_c_last_row(int64_t n, const int64_t *pd_rp, const int32_t *pd_col, int64_t ncl, int32_t *last,
                               cudaStream_t st);
 
+// deterministic owner-computes numeric pass (ptap_tile.cu)
+constexpr int TILE_ROWS = 64;      // fine rows per block (work item)
+constexpr int TILE_MAX_CROW = 64;  // widest C row the gather handles
+constexpr int TILE_GCAP = 512;     // contributor entries staged per gather chunk
+constexpr int TILE_MAXRUN = 16;    // runs of P rows staged per block
+struct TileArgs {
+  int32_t nloc, nblk, nitems, ring_blocks, blkcap, grid;  // nitems = nblk + ownership delay
+  int32_t napc;             // accumulator slots per row (>= widest AP row)
+  int32_t pstage;           // 1: stage the blocks' P runs in shared memory, 0: prefetch them into L1
+  int32_t sm_aval, sm_acol, sm_pstage, sm_prp, sm_acc, sm_meta, sm_tail, sm_total;  // dynamic shared memory layout (bytes)
+  const uint8_t *pr_n;      // [nblk] runs of P rows staged per block (0: read P from global memory)
+  const int2 *pr_k;         // [nblk * TILE_MAXRUN] run [k0, k1) of P rows
+  int32_t dbg;              // timing experiments only (PTAP_TILE_DBG): 1 no ring wait, 2 no flag wait, 4 no gather, 8 no fold
+  const uint16_t *ap_off;   // [nloc] AP row offset inside its block's ring slot (doubles)
+  double *ring;             // [ring_blocks * blkcap] AP rows of the blocks in flight
+  const int32_t *own_rp;    // [nitems + 1] first C row owned by each item (owners are non-decreasing)
+  const int64_t *qmap_rp;   // [ncl] gather map of each C row (interned pool offset)
+  const uint8_t *qmap;      // [contributor][position] -> AP slot, 0xff: none
+  const int32_t *t_rp;      // [ncl + 1] P_d^T: contributors of each C row
+  const int32_t *t_row;     // [nnz(P_d)] contributing fine rows, ascending per C row
+  const int32_t *t_pidx;    // [nnz(P_d)] index of P(i,J) in P_d's values
+  const uint8_t *t_jx;      // symbolic only: index of the entry inside the fine row's P row
+  const int32_t *rd_rp;     // [nblk + 1] distinct blocks each item's gathers read
+  const int32_t *rd_blk;
+  const uint32_t *expect;   // [nblk] readers of each block per pass
+  uint32_t *flags;          // [nblk] epoch in which the block's AP rows were published
+  uint32_t *readcnt;        // [nblk] reader signals, cumulative over passes
+  uint32_t *ctl;            // [0] ticket, [1] epoch
+};
+size_t tile_smem_layout(TileArgs &ta, int amax_blk, int pvmax, int prmax);
+int tile_grid(const TileArgs &ta);
+cudaError_t launch_tile_pruns(int nblk, int64_t nloc, const int64_t *ad_rp, const int32_t *ad_col,
+                              const int64_t *pd_rp, int64_t pnnz, int pvcap, int prcap, uint8_t *pr_n, int2 *pr_k,
+                              unsigned long long *stats, cudaStream_t st);
+size_t tile_scan_scratch(int64_t n);
+cudaError_t launch_tile_numeric(const Ops &op, const MapArgs &mp, const TileArgs &ta, const int64_t *c_rp,
+                                double *c_val, int blk_lo, int blk_hi, bool new_pass, cudaStream_t st);
+cudaError_t launch_tile_transpose(int64_t n, int64_t ncl, const int64_t *pd_rp, const int32_t *pd_col,
+                                  int64_t pnnz, int32_t *cnt, int32_t *t_rp, int32_t *cursor, int32_t *t_row,
+                                  uint8_t *t_jx, void *scratch, size_t scratch_bytes, int *status,
+                                  cudaStream_t st);
+size_t tile_owner_scratch(int64_t ncl);
+cudaError_t launch_tile_owners(int64_t ncl, int nblk, int delay, const int64_t *pd_rp, const int32_t *t_rp,
+                               int32_t *t_row, uint8_t *t_jx, int32_t *t_pidx, long long *key, int32_t *owner,
+                               unsigned long long *stats, void *scratch, size_t scratch_bytes, cudaStream_t st);
+cudaError_t launch_tile_own_rp(int nitems, int64_t ncl, const int32_t *owner, int32_t *own_rp, cudaStream_t st);
+cudaError_t launch_tile_apoff(int64_t n, const int64_t *ad_rp, const int64_t *pd_rp, const uint8_t *nap,
+                              uint16_t *ap_off, unsigned long long *stats, cudaStream_t st);
+cudaError_t launch_tile_reads(int pass, int nitems, int delay, int span, const int32_t *own_rp,
+                              const int32_t *t_rp, const int32_t *t_row, int32_t *rd_cnt,
+                              const int32_t *rd_rp, int32_t *rd_blk, uint32_t *expect, cudaStream_t st);
+cudaError_t launch_tile_qmap(int64_t ncl, const TileArgs &ta, const int64_t *c_rp, int64_t *qlen, int64_t *qm_rp,
+                             const uint8_t *nap, const int64_t *pmap_rp, const uint8_t *pmap, uint8_t *qm, int pass,
+                             cudaStream_t st);
+cudaError_t launch_tile_c_last(int64_t ncl, const TileArgs &ta, int32_t *last, cudaStream_t st);
+cudaError_t launch_tile_scan32(const int32_t *in, int32_t *out, int n, void *scratch, size_t scratch_bytes,
+                               cudaStream_t st);
+
 }  // namespace ptapdev

@@ -49,21 +49,32 @@ def _torch():
 
 
 class _CudaArray:
-    """Expose a library-owned device buffer to torch without copying."""
+    """Expose a library-owned device buffer to torch without copying.  The
+    tensor torch builds keeps this object alive, and this object keeps the
+    owning plan alive, so a view never outlives the plan's memory."""
 
     _TYPESTR = {"int64": "<i8", "int32": "<i4", "float64": "<f8"}
 
-    def __init__(self, ptr: int, n: int, dtype: str):
+    def __init__(self, ptr: int, n: int, dtype: str, owner=None):
+        self._owner = owner
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": self._TYPESTR[dtype],
                                          "data": (int(ptr or 0), False), "version": 3, "strides": None}
 
 
-def _dev_view(ptr, n, dtype, device):
+def _dev_view(ptr, n, dtype, device, owner=None):
     torch = _torch()
     tdt = {"int64": torch.int64, "int32": torch.int32, "float64": torch.float64}[dtype]
     if not ptr or n == 0:
         return torch.zeros(0, dtype=tdt, device=device)
-    return torch.as_tensor(_CudaArray(ptr, n, dtype), device=device)
+    return torch.as_tensor(_CudaArray(ptr, n, dtype, owner), device=device)
+
+
+def _want_deterministic(flag) -> bool:
+    """Explicit argument, else the PTAP_DETERMINISTIC environment switch."""
+    import os
+    if flag is None:
+        return os.environ.get("PTAP_DETERMINISTIC", "") not in ("", "0")
+    return bool(flag)
 
 
 def _stream_ptr():
@@ -179,15 +190,16 @@ class TripleProductPlan:
         v = _lib.CView()
         _lib.check(self._lib().ptap_plan_get_c(self._h, ctypes.byref(v)), "get C")
         dev = self._device
-        return (_dev_view(v.row_ptr, v.nrows + 1, "int64", dev), _dev_view(v.col, v.nnz, "int32", dev),
-                _dev_view(v.val, v.nnz, "float64", dev))
+        return (_dev_view(v.row_ptr, v.nrows + 1, "int64", dev, self), _dev_view(v.col, v.nnz, "int32", dev, self),
+                _dev_view(v.val, v.nnz, "float64", dev, self))
 
     def _staging_device(self):
         s = _lib.Staging()
         _lib.check(self._lib().ptap_plan_staging(self._h, ctypes.byref(s)), "staging")
         dev = self._device
-        return (_dev_view(s.rows, s.nrows, "int32", dev), _dev_view(s.row_ptr, s.nrows + 1 if s.nrows else 0, "int64", dev),
-                _dev_view(s.col, s.nnz, "int32", dev), _dev_view(s.val, s.nnz, "float64", dev))
+        return (_dev_view(s.rows, s.nrows, "int32", dev, self),
+                _dev_view(s.row_ptr, s.nrows + 1 if s.nrows else 0, "int64", dev, self),
+                _dev_view(s.col, s.nnz, "int32", dev, self), _dev_view(s.val, s.nnz, "float64", dev, self))
 
     @property
     def c_alloc(self) -> AllocatedMatrix:
@@ -266,6 +278,16 @@ class TripleProductPlan:
         except Exception:
             pass
 
+    @property
+    def deterministic(self) -> bool:
+        """True when repeated numeric passes are bitwise identical: the
+        two-step comparator, or an all-at-once / merged plan running the
+        owner-computes kernel (numeric_path 2; ``deterministic=True`` at
+        symbolic time on a one-rank-structured local loop)."""
+        if self.algorithm == TWO_STEP:
+            return True
+        return bool(self._h) and self.device_counters()["numeric_path"] == 2
+
     # two-step inspection helpers (reference plan.ctilde / pt_d / pt_o)
     @property
     def ctilde(self):
@@ -326,7 +348,7 @@ def _remote_csr(rr: RemoteRows, m: int, device) -> DeviceCsr:
 # ---------------------------------------------------------------------------
 
 
-def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str) -> TripleProductPlan:
+def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str, deterministic=None) -> TripleProductPlan:
     _check_triple_operands(a, p)
     L = _lib.load()
     torch = _torch()
@@ -350,6 +372,8 @@ def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str) ->
         st = ops.struct()
         _lib.check(L.ptap_plan_create(_lib.ALGORITHM_CODES[algorithm], ctypes.byref(st), ctypes.byref(plan._h)),
                    "plan create")
+        if _want_deterministic(deterministic):
+            _lib.check(L.ptap_plan_set_option(plan._h, b"deterministic", 1), "plan option")
         stream = _stream_ptr()
         _lib.check(L.ptap_symbolic_send(plan._h, ctypes.byref(st), stream), "symbolic send")
         s_rows, s_rp, s_col, _ = plan._staging_device()
@@ -428,7 +452,9 @@ def _numeric_streamed(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx
     nblk = max(1, int(os.environ.get("PTAP_UPLOAD_BLOCKS", _UPLOAD_BLOCKS)))
     n = a.local.nrows
     a_rp = a.local.diag.row_offsets
-    bounds = [n * k // nblk for k in range(nblk + 1)]
+    # block-aligned bounds (the plan's numeric kernels fold 64-row blocks)
+    bounds = [min(n, -(-(n * k // nblk) // 64) * 64) for k in range(nblk + 1)]
+    bounds[-1] = n
     a_host = torch.from_numpy(a.local.diag.values)
     p_host = torch.from_numpy(p.local.diag.values)
     a_dev, p_dev = plan._a_dev.diag.val, plan._p_dev.diag.val
@@ -518,9 +544,12 @@ def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankCon
     return plan.c_local() if to_host else plan.c_device()
 
 
-def aao_symbolic(a, p, ctx) -> TripleProductPlan:
-    """All-at-once symbolic: send loop, exchange, local loop (Alg. 7)."""
-    return _symbolic(a, p, ctx, ALL_AT_ONCE)
+def aao_symbolic(a, p, ctx, *, deterministic=None) -> TripleProductPlan:
+    """All-at-once symbolic: send loop, exchange, local loop (Alg. 7).
+    ``deterministic=True`` (or PTAP_DETERMINISTIC=1) selects the
+    owner-computes numeric kernel: bitwise-repeatable passes whose C is
+    bit-identical to the reference's at one rank."""
+    return _symbolic(a, p, ctx, ALL_AT_ONCE, deterministic)
 
 
 def aao_numeric(a, p, plan, ctx):
@@ -528,18 +557,19 @@ def aao_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, ALL_AT_ONCE)
 
 
-def merged_symbolic(a, p, ctx) -> TripleProductPlan:
+def merged_symbolic(a, p, ctx, *, deterministic=None) -> TripleProductPlan:
     """Merged all-at-once: one fused loop computes each AP row once (Alg. 9)."""
-    return _symbolic(a, p, ctx, MERGED)
+    return _symbolic(a, p, ctx, MERGED, deterministic)
 
 
 def merged_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, MERGED)
 
 
-def two_step_symbolic(a, p, ctx) -> TripleProductPlan:
-    """Two-step: C~ = A P, explicit P^T, then P^T C~ (Alg. 5)."""
-    return _symbolic(a, p, ctx, TWO_STEP)
+def two_step_symbolic(a, p, ctx, *, deterministic=None) -> TripleProductPlan:
+    """Two-step: C~ = A P, explicit P^T, then P^T C~ (Alg. 5); always
+    deterministic (every entry is folded in the reference's order)."""
+    return _symbolic(a, p, ctx, TWO_STEP, deterministic)
 
 
 def two_step_numeric(a, p, plan, ctx):
@@ -550,10 +580,10 @@ _SYMBOLIC = {TWO_STEP: two_step_symbolic, ALL_AT_ONCE: aao_symbolic, MERGED: mer
 _NUMERIC = {TWO_STEP: two_step_numeric, ALL_AT_ONCE: aao_numeric, MERGED: merged_numeric}
 
 
-def run_symbolic(a, p, algorithm: str, ctx) -> TripleProductPlan:
+def run_symbolic(a, p, algorithm: str, ctx, *, deterministic=None) -> TripleProductPlan:
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
-    return _SYMBOLIC[algorithm](a, p, ctx)
+    return _SYMBOLIC[algorithm](a, p, ctx, deterministic=deterministic)
 
 
 def run_numeric(a, p, plan: TripleProductPlan, ctx):
@@ -565,11 +595,12 @@ def run_numeric_device(a, p, plan: TripleProductPlan, ctx):
     return _numeric(a, p, plan, ctx, plan.algorithm, to_host=False)
 
 
-def ptap(a: DistMatrix, p: DistMatrix, algorithm: str, ctx: RankContext, cache: str = CACHE_KEEP):
+def ptap(a: DistMatrix, p: DistMatrix, algorithm: str, ctx: RankContext, cache: str = CACHE_KEEP, *,
+         deterministic=None):
     """One symbolic plus one numeric triple product; returns (C, plan)."""
     if cache not in (CACHE_KEEP, CACHE_FREE):
         raise ValueError(f"cache policy must be '{CACHE_KEEP}' or '{CACHE_FREE}'")
-    plan = run_symbolic(a, p, algorithm, ctx)
+    plan = run_symbolic(a, p, algorithm, ctx, deterministic=deterministic)
     local = run_numeric(a, p, plan, ctx)
     if cache == CACHE_FREE:
         plan.release_cache(ctx)
