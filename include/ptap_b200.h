@@ -180,10 +180,12 @@ ptap_status ptap_numeric_send(ptap_plan *plan, const ptap_operands *ops, void *s
 ptap_status ptap_numeric_local(ptap_plan *plan, const ptap_operands *ops, void *stream);
 ptap_status ptap_numeric_merge(ptap_plan *plan, const double *recv_vals, void *stream);
 /* All-at-once local loop over the fine rows [row_lo, row_hi) only, so a
- * caller can fold row blocks as their A values arrive (flags bit 0: zero C
- * first; bit 1: also run the rows outside the range-addressable bin -- pass
- * it on the last block).  Returns PTAP_ERR_VALUE when the plan's local rows
- * are not one range-addressable bin (callers then use ptap_numeric_local). */
+ * caller can fold row blocks as their A values arrive (flags bit 0: first
+ * block of the pass -- zero C / open a new epoch; bit 1: last block of the
+ * pass, counted as one numeric run).  Ranges are aligned to 64-row blocks
+ * (the last may end at n_local).  Returns PTAP_ERR_VALUE when the plan's
+ * local rows are not one range-addressable bin (callers then use
+ * ptap_numeric_local). */
 ptap_status ptap_numeric_local_rows(ptap_plan *plan, const ptap_operands *ops, int64_t row_lo, int64_t row_hi,
                                     int flags, void *stream);
 /* last[J] (device, int32, one per local C row) = the largest local fine row
@@ -192,6 +194,15 @@ ptap_status ptap_numeric_local_rows(ptap_plan *plan, const ptap_operands *ops, i
 ptap_status ptap_plan_c_last_row(ptap_plan *plan, const ptap_operands *ops, int32_t *last, void *stream);
 /* Synchronise and report device-side drift detected by the last numeric pass. */
 ptap_status ptap_plan_check(ptap_plan *plan, void *stream);
+/* Full structural check (reference verify_filled, src/spgemm.py:58-68, and the
+ * CRC32 token of src/comm.py:517-524): digest of every structure array of the
+ * operands against the symbolic-time digest; PTAP_ERR_DRIFT on mismatch.
+ * (Every numeric call already checks sizes, and re-digests when a structure
+ * array was replaced by another buffer.)  Synchronises. */
+ptap_status ptap_plan_verify(ptap_plan *plan, const ptap_operands *ops, void *stream);
+/* Two-step only: the stored auxiliary C~ = A P (reference plan.ctilde,
+ * src/tripleproduct.py:105-145), rows of the rank, global columns. */
+ptap_status ptap_plan_get_ctilde(ptap_plan *plan, ptap_c_view *out);
 
 ptap_status ptap_plan_get_c(ptap_plan *plan, ptap_c_view *out);
 ptap_status ptap_plan_release_cache(ptap_plan *plan);

@@ -35,6 +35,8 @@ ptap_status fail(ptap_status s, const std::string &msg) {
 
 enum Cat { CAT_INPUT = 0, CAT_OUTPUT = 1, CAT_AUX = 2, CAT_TRANSIENT = 3, CAT_PLAN = 4 };
 
+cudaMemPool_t lib_pool();
+
 // PTAP_TRACE=1: synchronise and print the wall time of each symbolic step
 struct Tracer {
   bool on = getenv("PTAP_TRACE") != nullptr;
@@ -44,12 +46,9 @@ struct Tracer {
     cudaStreamSynchronize(st);
     auto t1 = std::chrono::steady_clock::now();
     unsigned long long reserved = 0, used = 0;
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    }
+    cudaMemPool_t pool = lib_pool();
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
     fprintf(stderr, "[ptap] %-28s %9.3f ms   pool reserved %.2f GB used %.2f GB\n", what,
             std::chrono::duration<double, std::milli>(t1 - t0).count(), reserved / 1e9, used / 1e9);
     t0 = t1;
@@ -119,6 +118,10 @@ struct ptap_plan {
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
   bool tile = false;                // ... and the deterministic owner-computes kernel replaces it
   bool deterministic = false;       // plan option: bitwise-repeatable numeric passes (tile kernel)
+  // symbolic-time image of the operands' structure (drift detection)
+  int64_t img_shape[11] = {0};
+  const void *img_ptr[11] = {nullptr};
+  unsigned long long img_digest = 0;
   TileArgs ta{};
   int64_t max_nap = 0;              // widest AP row
   int64_t qmap_bytes = 0;           // tile gather maps (interned)
@@ -160,11 +163,52 @@ struct ptap_plan {
 
 namespace {
 
+// The library's own stream-ordered pool (not the device default pool, which
+// torch and NCCL may use): freed plan memory is kept for the next symbolic
+// phase, and release_cache / plan destroy trim it back to the driver.
+// PTAP_POOL_RESERVE_GB maps a block up front (opt-in).
+cudaMemPool_t lib_pool() {
+  static cudaMemPool_t pool = nullptr;
+  static int pool_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (pool && pool_dev == dev) return pool;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    cudaDeviceGetDefaultMemPool(&pool, dev);
+  }
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  pool_dev = dev;
+  const char *rv = getenv("PTAP_POOL_RESERVE_GB");
+  const double gb = rv ? atof(rv) : 0.0;
+  if (gb > 0) {
+    void *ptr = nullptr;
+    if (cudaMallocFromPoolAsync(&ptr, (size_t)(gb * 1073741824.0), pool, 0) == cudaSuccess) {
+      cudaFreeAsync(ptr, 0);
+      cudaStreamSynchronize(0);
+    }
+    cudaGetLastError();
+  }
+  return pool;
+}
+
+void trim_pool() {
+  cudaMemPoolTrimTo(lib_pool(), 0);
+}
+
+int g_live_plans = 0;
+
 ptap_status palloc_raw(ptap_plan *p, void **out, size_t bytes, int cat, cudaStream_t st) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~size_t(255);
   void *ptr = nullptr;
-  cudaError_t e = cudaMallocAsync(&ptr, bytes, st);
+  cudaError_t e = cudaMallocFromPoolAsync(&ptr, bytes, lib_pool(), st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? PTAP_ERR_OOM : PTAP_ERR_CUDA,
@@ -232,6 +276,63 @@ ptap_status validate(const ptap_operands *o) {
     return fail(PTAP_ERR_DRIFT, "gathered rows do not match A's off-diagonal columns");
   if (o->p_off.nnz > 0 && (o->p_off.nrows != o->n_local || o->p_off.ncols != o->p_colmap_len))
     return fail(PTAP_ERR_PARTITION, "P's off-diagonal block does not match its column map");
+  return PTAP_OK;
+}
+
+void op_shape(const ptap_operands *o, int64_t *sh, const void **pt) {
+  const int64_t v[11] = {o->n_local, o->m_global, o->c_lo, o->c_hi, o->a_diag.nnz, o->a_off.nnz, o->p_diag.nnz,
+                         o->p_off.nnz, o->p_colmap_len, o->p_remote.nrows, o->p_remote.nnz};
+  for (int k = 0; k < 11; ++k) sh[k] = v[k];
+  const void *q[11] = {o->a_diag.row_ptr, o->a_diag.col, o->a_off.row_ptr, o->a_off.col, o->p_diag.row_ptr,
+                       o->p_diag.col, o->p_off.row_ptr, o->p_off.col, o->p_colmap, o->p_remote.row_ptr,
+                       o->p_remote.col};
+  if (pt)
+    for (int k = 0; k < 11; ++k) pt[k] = q[k];
+}
+
+// digest of every structure array of the operands (row offsets, columns,
+// column map): one pass over 1.9 GB on config 3 level 1, synchronous
+ptap_status op_digest(ptap_plan *p, const ptap_operands *o, cudaStream_t st, unsigned long long *out) {
+  unsigned long long *d = p->d_u64 + 23;
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+  const ptap_csr *blocks[5] = {&o->a_diag, &o->a_off, &o->p_diag, &o->p_off, &o->p_remote};
+  for (int k = 0; k < 5; ++k) {
+    const ptap_csr &c = *blocks[k];
+    if (c.nnz > 0) {
+      CK(launch_digest_i64(c.row_ptr, c.nrows + 1, 2 * k + 1, d, st));
+      CK(launch_digest_i32(c.col, c.nnz, 2 * k + 2, d, st));
+    }
+  }
+  if (o->p_colmap_len > 0) CK(launch_digest_i32(o->p_colmap, o->p_colmap_len, 11, d, st));
+  CK(cudaMemcpyAsync(out, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PTAP_OK;
+}
+
+ptap_status record_image(ptap_plan *p, const ptap_operands *o, cudaStream_t st) {
+  op_shape(o, p->img_shape, p->img_ptr);
+  return op_digest(p, o, st, &p->img_digest);
+}
+
+// every numeric call: the operands' shape must be the symbolic one (the
+// kernels trust the plan's maps); when the structure arrays were swapped
+// for other buffers, their contents must digest to the symbolic image
+// (reference: CRC32 structure token, src/comm.py:517-524, and the fill
+// checks of src/spgemm.py:54-68)
+ptap_status check_image(ptap_plan *p, const ptap_operands *o, cudaStream_t st) {
+  int64_t sh[11];
+  const void *pt[11];
+  op_shape(o, sh, pt);
+  for (int k = 0; k < 11; ++k)
+    if (sh[k] != p->img_shape[k])
+      return fail(PTAP_ERR_DRIFT, "operand structure changed since the symbolic phase (sizes differ)");
+  bool same = true;
+  for (int k = 0; k < 11; ++k) same = same && pt[k] == p->img_ptr[k];
+  if (same) return PTAP_OK;
+  unsigned long long dg = 0;
+  CKS(op_digest(p, o, st, &dg));
+  if (dg != p->img_digest) return fail(PTAP_ERR_DRIFT, "operand structure changed since the symbolic phase");
+  for (int k = 0; k < 11; ++k) p->img_ptr[k] = pt[k];
   return PTAP_OK;
 }
 
@@ -1233,35 +1334,8 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
   if (!out) return fail(PTAP_ERR_VALUE, "null output");
   if (algorithm < 0 || algorithm > 2) return fail(PTAP_ERR_VALUE, "unknown algorithm");
   CKS(validate(ops));
-  static bool pool_configured = false;
-  if (!pool_configured) {
-    // keep freed device memory in the stream-ordered pool: repeated symbolic
-    // phases reuse it instead of going back to the driver
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      // map a block up front (PTAP_POOL_RESERVE_GB, default 8 GB on a device
-      // of >= 64 GB, 0 disables): the symbolic phase's large buffers then do
-      // not wait for the driver to map new physical memory (measured: cfg3
-      // prepare_maps 4-16 ms -> 4 ms steady)
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      const char *rv = getenv("PTAP_POOL_RESERVE_GB");
-      const double gb = rv ? atof(rv) : (tot >= (size_t(64) << 30) ? 8.0 : 0.0);
-      if (gb > 0) {
-        void *ptr = nullptr;
-        if (cudaMallocAsync(&ptr, (size_t)(gb * 1073741824.0), 0) == cudaSuccess) {
-          cudaFreeAsync(ptr, 0);
-          cudaStreamSynchronize(0);
-        }
-      }
-    }
-    cudaGetLastError();
-    pool_configured = true;
-  }
   ptap_plan *p = new ptap_plan();
+  ++g_live_plans;
   p->alg = algorithm;
   p->nloc = ops->n_local;
   p->m = ops->m_global;
@@ -1274,6 +1348,7 @@ ptap_status ptap_plan_create(int algorithm, const ptap_operands *ops, ptap_plan 
   if (e == cudaSuccess) e = cudaMemset(p->d_status, 0, sizeof(int));
   if (e != cudaSuccess) {
     delete p;
+    --g_live_plans;
     return fail(PTAP_ERR_CUDA, std::string("plan create: ") + cudaGetErrorString(e));
   }
   *out = p;
@@ -1297,6 +1372,9 @@ ptap_status ptap_plan_destroy(ptap_plan *p) {
   cudaFree(p->d_status);
   cudaFree(p->d_u64);
   delete p;
+  // the last plan gone: give the pool's memory back to the driver (torch,
+  // NCCL), unless PTAP_POOL_KEEP asks to keep it for the next plan
+  if (--g_live_plans <= 0 && !getenv("PTAP_POOL_KEEP")) trim_pool();
   return PTAP_OK;
 }
 
@@ -1304,6 +1382,7 @@ ptap_status ptap_symbolic_send(ptap_plan *p, const ptap_operands *ops, void *str
   if (!p) return fail(PTAP_ERR_VALUE, "null plan");
   CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
+  CKS(record_image(p, ops, st));
   Ops op = make_ops(ops);
   Tracer tr;
   if (p->nloc > 0) p->avg_p_row = (double)(ops->p_diag.nnz + ops->p_off.nnz) / (double)p->nloc;
@@ -1549,6 +1628,7 @@ ptap_status ptap_numeric_send(ptap_plan *p, const ptap_operands *ops, void *stre
   CKS(numeric_ready(p));
   CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
+  CKS(check_image(p, ops, st));
   Ops op = make_ops(ops);
   if (p->alg == PTAP_TWO_STEP) {
     CKS(for_bins(p, p->bins_all, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
@@ -1578,6 +1658,7 @@ ptap_status ptap_numeric_local(ptap_plan *p, const ptap_operands *ops, void *str
   CKS(numeric_ready(p));
   CKS(validate(ops));
   cudaStream_t st = (cudaStream_t)stream;
+  CKS(check_image(p, ops, st));
   Ops op = make_ops(ops);
   if (p->alg == PTAP_TWO_STEP) {
     PtcTarget tg{0, p->ncl, nullptr, p->c_rp, p->c_col, p->c_val};
@@ -1604,6 +1685,7 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
     return fail(PTAP_ERR_VALUE, "plan has no range-addressable local rows");
   if (row_lo < 0 || row_hi > p->nloc || row_lo > row_hi) return fail(PTAP_ERR_VALUE, "row range");
   cudaStream_t st = (cudaStream_t)stream;
+  CKS(check_image(p, ops, st));
   Ops op = make_ops(ops);
   if (p->tile) {
     // block-aligned ranges (the last may end at nloc); the first call of a
@@ -1664,6 +1746,36 @@ ptap_status ptap_plan_check(ptap_plan *p, void *stream) {
   return status_to_error(s, "numeric");
 }
 
+ptap_status ptap_plan_verify(ptap_plan *p, const ptap_operands *ops, void *stream) {
+  CKS(numeric_ready(p));
+  CKS(validate(ops));
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t sh[11];
+  op_shape(ops, sh, nullptr);
+  for (int k = 0; k < 11; ++k)
+    if (sh[k] != p->img_shape[k])
+      return fail(PTAP_ERR_DRIFT, "operand structure changed since the symbolic phase (sizes differ)");
+  unsigned long long dg = 0;
+  CKS(op_digest(p, ops, st, &dg));
+  if (dg != p->img_digest) return fail(PTAP_ERR_DRIFT, "operand structure changed since the symbolic phase");
+  int s = 0;
+  CKS(read_status(p, st, &s));
+  return status_to_error(s, "numeric");
+}
+
+ptap_status ptap_plan_get_ctilde(ptap_plan *p, ptap_c_view *out) {
+  if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
+  if (p->alg != PTAP_TWO_STEP) return fail(PTAP_ERR_VALUE, "only a two-step plan stores C~ = A P");
+  if (p->released) return fail(PTAP_ERR_DRIFT, "plan internals were released (free-after-solve); rebuild the plan");
+  out->nrows = p->nloc;
+  out->ncols = p->m;
+  out->nnz = p->ct_nnz;
+  out->row_ptr = p->ct_rp;
+  out->col = p->ct_col;
+  out->val = p->ct_val;
+  return PTAP_OK;
+}
+
 ptap_status ptap_plan_get_c(ptap_plan *p, ptap_c_view *out) {
   if (!p || !out) return fail(PTAP_ERR_VALUE, "null argument");
   out->nrows = p->ncl;
@@ -1693,6 +1805,7 @@ ptap_status ptap_plan_release_cache(ptap_plan *p) {
     pfree(p, t->rp, st); pfree(p, t->row, st); pfree(p, t->perm, st); pfree(p, t->val, st);
   }
   cudaStreamSynchronize(st);
+  trim_pool();
   p->released = true;
   return PTAP_OK;
 }

@@ -1636,6 +1636,33 @@ cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const Map
   return cudaGetLastError();
 }
 
+// order-independent digest of an index array (position-sensitive): sum of
+// mix(salt, i, v) over the entries, wrapping
+__device__ __forceinline__ unsigned long long dg_mix(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+template <typename T>
+__global__ void k_digest(const T *a, int64_t n, unsigned long long salt, unsigned long long *out) {
+  unsigned long long h = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    h += dg_mix((salt << 58) ^ ((unsigned long long)i << 24) ^ dg_mix((unsigned long long)(long long)a[i]));
+  for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(FULL, h, o);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(out, h);
+}
+cudaError_t launch_digest_i64(const int64_t *a, int64_t n, unsigned long long salt, unsigned long long *out,
+                              cudaStream_t st) {
+  if (n > 0 && a) k_digest<int64_t><<<148 * 8, 256, 0, st>>>(a, n, salt, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_digest_i32(const int32_t *a, int64_t n, unsigned long long salt, unsigned long long *out,
+                              cudaStream_t st) {
+  if (n > 0 && a) k_digest<int32_t><<<148 * 8, 256, 0, st>>>(a, n, salt, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_touch(void *buf, int64_t bytes, cudaStream_t st) {
   int64_t n = bytes / 16;
   k_touch<<<148 * 8, 256, 0, st>>>((int4 *)buf, n);

@@ -144,6 +144,10 @@ cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t tar
                            int64_t t_nrows, const int32_t *t_rows, const int64_t *t_rp, int64_t *est,
                            cudaStream_t st);
 cudaError_t launch_touch(void *buf, int64_t bytes, cudaStream_t st);
+cudaError_t launch_digest_i64(const int64_t *a, int64_t n, unsigned long long salt, unsigned long long *out,
+                              cudaStream_t st);
+cudaError_t launch_digest_i32(const int32_t *a, int64_t n, unsigned long long salt, unsigned long long *out,
+                              cudaStream_t st);
 cudaError_t launch_map_lengths(int64_t n, const int64_t *pd_rp, const int64_t *po_rp, const int64_t *apub,
                                const int64_t *ap_nnz, int64_t *slen, int64_t *plen, cudaStream_t st);
 cudaError_t launch_po_srow(int64_t nnz, const int32_t *po_col, const int32_t *colmap, int64_t s_nrows,

@@ -66,8 +66,13 @@ class DeviceCsr:
             src = values
         else:
             src = torch.from_numpy(np.ascontiguousarray(values, np.float64))
-        if self.val is None or self.val.numel() != src.numel():
+        if self.val is None:
             self.val = src.to(self.row_ptr.device, non_blocking=non_blocking)
+        elif self.val.numel() != src.numel():
+            # a plan built on this block sized every map for its nnz
+            from .errors import StructuralDriftError
+            raise StructuralDriftError(
+                f"value array has {src.numel()} entries, the block's structure has {self.val.numel()}")
         else:
             self.val.copy_(src, non_blocking=non_blocking)
 

@@ -14,7 +14,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .comm import RankContext, gather_remote_rows
+from .comm import RankContext, gather_remote_rows, refresh_remote_values
 from .device import DeviceCsr, DeviceLocalMatrix, DeviceOperands
 from .errors import PartitionMismatchError
 from .partition import DistMatrix, LocalMatrix
@@ -76,13 +76,25 @@ def symbolic_ap(a: DistMatrix, p: DistMatrix, ctx: RankContext) -> DeviceAP:
 
 
 def numeric_ap(a: DistMatrix, p: DistMatrix, c: DeviceAP, ctx: RankContext) -> DeviceAP:
+    """Values of C~ = A*P into the symbolic structure (reference numeric_ap,
+    src/spgemm.py:205-234): the operands' current values -- host operands
+    are uploaded, device operands are used as given -- and, at several
+    ranks, the gathered rows of P refreshed first (values only,
+    update_remote_rows_numeric, src/spgemm.py:224-225)."""
     torch = _torch()
     L = _lib.load()
     ops = c._ops
     if isinstance(a.local, LocalMatrix):
         ops.a.refresh_values(a.local)
+    else:
+        ops.a = a.local
     if isinstance(p.local, LocalMatrix):
         ops.p.refresh_values(p.local)
+    else:
+        ops.p = p.local
+    if ctx.nranks > 1:
+        refresh_remote_values(ctx, c._remote, ops.p)
+        ops.p_remote.val = c._remote.val
     st = ops.struct()
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     _lib.check(L.ptap_spgemm_ap_numeric(ctypes.byref(st), ctypes.c_void_p(c.row_ptr.data_ptr()),

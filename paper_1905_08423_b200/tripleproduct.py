@@ -85,13 +85,24 @@ def _stream_ptr():
 @dataclass
 class AllocatedMatrix:
     """Host view of the allocated C (reference AllocatedMatrix,
-    src/spgemm.py:35-68).  ``local`` is refreshed by every numeric pass."""
+    src/spgemm.py:35-68).  ``local`` is refreshed by every numeric pass.
+
+    The reference marks every slot a numeric pass writes (fill flags) and
+    raises StructuralDriftError when one was never written -- i.e. when the
+    operands' structure no longer matches the symbolic plan.  On the device
+    the numeric kernels write C through the plan's maps, so the same
+    condition is checked at its source: every numeric call compares the
+    operands' sizes with the symbolic image (and re-digests replaced
+    structure arrays); ``verify_filled`` runs the full device digest of every
+    structure array against the symbolic one (``ptap_plan_verify``).  The
+    fill arrays report the slots the last verified pass wrote."""
 
     local: LocalMatrix
     nzd: np.ndarray
     nzo: np.ndarray
     fill_d: np.ndarray
     fill_o: np.ndarray
+    _plan: object = None
 
     @property
     def nbytes(self) -> int:
@@ -101,10 +112,14 @@ class AllocatedMatrix:
         self.fill_d[:] = 0
         self.fill_o[:] = 0
 
-    def verify_filled(self, what: str):
-        # every slot is written on the device (C is zeroed then accumulated, or
-        # written from the row table); drift is detected by the kernels
-        return None
+    def verify_filled(self, what: str = "C"):
+        plan = self._plan
+        if plan is None or not plan._h or plan._ops is None:
+            raise StructuralDriftError(f"{what}: no live plan to verify against")
+        st = plan._ops.struct()
+        _lib.check(_lib.load().ptap_plan_verify(plan._h, ctypes.byref(st), _stream_ptr()), f"verify {what}")
+        self.fill_d[:] = 1
+        self.fill_o[:] = 1
 
 
 @dataclass
@@ -228,7 +243,8 @@ class TripleProductPlan:
         off = CsrMatrix(n, col_map.size, ipo, np.searchsorted(col_map, col[~inside]), np.zeros(off_idx.size), check=False)
         local = LocalMatrix(c_lo, c_hi, c_lo, c_hi, diag, off, col_map)
         self._c_host = (diag_idx, off_idx)
-        self._c_alloc = AllocatedMatrix(local, nzd, nzo, np.ones(diag_idx.size, np.uint8), np.ones(off_idx.size, np.uint8))
+        self._c_alloc = AllocatedMatrix(local, nzd, nzo, np.ones(diag_idx.size, np.uint8), np.ones(off_idx.size, np.uint8),
+                                        self)
 
     def c_local(self) -> LocalMatrix:
         """Copy the current C values to the host LocalMatrix view."""
@@ -288,10 +304,20 @@ class TripleProductPlan:
             return True
         return bool(self._h) and self.device_counters()["numeric_path"] == 2
 
-    # two-step inspection helpers (reference plan.ctilde / pt_d / pt_o)
+    # two-step inspection helper (reference plan.ctilde)
     @property
     def ctilde(self):
-        return None if self.algorithm != TWO_STEP or self.released else True
+        """Two-step: the stored auxiliary C~ = A P of this rank as device
+        tensors (row_ptr int64, col int32 global, val float64), or None
+        (other algorithms, or after release_cache)."""
+        if self.algorithm != TWO_STEP or self.released or not self._h:
+            return None
+        v = _lib.CView()
+        _lib.check(self._lib().ptap_plan_get_ctilde(self._h, ctypes.byref(v)), "ctilde")
+        dev = self._device
+        from .spgemm import DeviceAP
+        return DeviceAP(_dev_view(v.row_ptr, v.nrows + 1, "int64", dev, self), _dev_view(v.col, v.nnz, "int32", dev, self),
+                        _dev_view(v.val, v.nnz, "float64", dev, self), v.ncols, None, None)
 
 
 # ---------------------------------------------------------------------------
@@ -318,9 +344,7 @@ def _prepare(plan: TripleProductPlan, a: DistMatrix, p: DistMatrix, ctx: RankCon
         return
     for which, m, tok in (("A", a, plan._a_token), ("P", p, plan._p_token)):
         if isinstance(m.local, LocalMatrix):
-            # same (frozen) structure arrays as at symbolic time: no hashing needed
-            if tok is not None and _identity(m.local) != tok[0] and structure_token(m.local) != tok[1]:
-                raise StructuralDriftError(f"{which} changed structure since the symbolic phase")
+            _check_host_structure(which, m.local, tok)
             target = plan._a_dev if which == "A" else plan._p_dev
             target.refresh_values(m.local)
         else:
@@ -334,8 +358,24 @@ def _prepare(plan: TripleProductPlan, a: DistMatrix, p: DistMatrix, ctx: RankCon
 
 
 def _identity(lm: LocalMatrix) -> tuple:
-    return tuple(id(x) for x in (lm.diag.row_offsets, lm.diag.col_indices, lm.offdiag.row_offsets,
-                                 lm.offdiag.col_indices, lm.col_map))
+    """The structure arrays themselves (strong references: their identity
+    cannot be recycled while the plan holds them)."""
+    return (lm.diag.row_offsets, lm.diag.col_indices, lm.offdiag.row_offsets, lm.offdiag.col_indices, lm.col_map)
+
+
+def _check_host_structure(which: str, lm: LocalMatrix, tok):
+    """Numeric-time drift check of a host operand: the very arrays seen at
+    symbolic time, still frozen (CsrMatrix makes its structure read-only),
+    need no hashing; anything else is compared by CRC (the reference's
+    structure token, src/comm.py:517-524)."""
+    if tok is None:
+        return
+    cur = _identity(lm)
+    # the CSR structure arrays are frozen by CsrMatrix; col_map is compared by identity
+    same = all(x is y for x, y in zip(cur, tok[0])) and not any(
+        getattr(x, "flags", None) is not None and x.flags.writeable for x in cur[:4])
+    if not same and (tok[1] is None or structure_token(lm) != tok[1]):
+        raise StructuralDriftError(f"{which} changed structure since the symbolic phase")
 
 
 def _remote_csr(rr: RemoteRows, m: int, device) -> DeviceCsr:
@@ -435,8 +475,7 @@ def _numeric_streamed(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx
     L = _lib.load()
     # drift check as in _prepare
     for which, m, tok in (("A", a, plan._a_token), ("P", p, plan._p_token)):
-        if tok is not None and _identity(m.local) != tok[0] and structure_token(m.local) != tok[1]:
-            raise StructuralDriftError(f"{which} changed structure since the symbolic phase")
+        _check_host_structure(which, m.local, tok)
     st = plan._ops.struct()
     dev = ctx.device
     if getattr(plan, "_stream_state", None) is None:
