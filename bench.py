@@ -5,10 +5,11 @@
 
 A step is one numeric C = P^T A P pass (plan reused: the paper's 1 symbolic +
 11 numeric protocol) on the 27-point random 256^3 operator with
-trilinear P to 128^3 (config 3 level 1; z-slab row blocks over N GPUs,
-torchrun one process per GPU over NCCL).  Inputs are generated on the device
-and are larger than L2 (A alone is 5.5 GB), so no flush is needed between
-steps.  The line reports:
+trilinear P to 128^3 (config 3 level 1; z-slab row blocks over N GPUs, one
+process per GPU over NCCL).  ``--gpus N`` without a torchrun environment
+re-launches itself under torch.distributed.run with N ranks.  Inputs are
+generated on the device and are larger than L2 (A alone is 5.5 GB), so no
+flush is needed between steps.  The line reports:
 
   value      GFLOP/s of the all-at-once numeric pass, 2 flops per multiply-add
              of the triple product (MAC_AP + MAC_outer), whole job
@@ -16,12 +17,18 @@ steps.  The line reports:
              buffers: H2D of the step's A/P values, D2H of C's values
   roofline   HBM: algorithmic bytes (A + P + C in the device layout) per launch
              of the fused numeric kernel / its CUDA-event time vs MEASURED_PEAKS
-  variants   merged and two-step numeric times, symbolic times, aux memory
-  cpu_baseline  the CPU oracle port (oracle/) on a bounded sample, rank 0, N=1
+  variants   merged, two-step and the deterministic (owner-computes) pass,
+             symbolic times (median of 5 warm runs), aux memory
+  cpu_baseline  the CPU oracle port (oracle/, the reference's algorithm in C)
+             on the SAME full workload, 1 thread, R = 1 (rank 0, N = 1); its C
+             is also compared with the GPU's C (full-size parity)
+  reference_numba  the reference package itself (numba, baseline/_ref) on
+             config 2 at np=1, with the port checked bit for bit against it
 
-``--impl reference`` times the reference algorithm on the host cores instead
-(the C port of the reference in oracle/, one simulated rank per thread; the
-reference itself is Python and cannot travel to the GPU box).
+``--impl reference`` times the reference algorithm on all host cores on the
+same full workload (the C port of the reference in oracle/, one simulated
+rank per thread; the reference itself is Python + numba and single-threaded,
+its own speed is recorded by the reference_numba leg).
 """
 
 from __future__ import annotations
@@ -30,6 +37,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,7 +47,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PtAP GFLOP/s & achieved HBM GB/s at 1/2/4/8 B200; peak auxiliary memory"
 UNIT = "GFLOP/s"
-SAMPLE_PLANES = 32  # CPU sample: fine z-planes [0, 32) of config 3 level 1
 
 
 def parse():
@@ -51,11 +58,31 @@ def parse():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--n-fine", type=int, default=None, help="override grid size (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-numba", action="store_true", help="skip the reference-package (numba) leg")
+    ap.add_argument("--numba-config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch/rendezvous only: every rank joins, rank 0 prints the line skeleton (CPU tests)")
     ap.add_argument("--csv", default=None, help="also write the reference bench's CSV columns (src/bench.py:43-56) "
                                                   "plus GFLOP/s, GB/s and roofline, one row per algorithm")
     return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# multi-rank launch (reference: src/cli.py:39 turns --ranks into N ranks)
+# ---------------------------------------------------------------------------
+def relaunch_distributed(args) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N processes (one per GPU, NCCL; PTAP_BACKEND=gloo for CPU checks)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -124,7 +151,7 @@ def measured_peak_hbm():
 
 def ncu_traffic():
     """dram bytes per launch of the fused numeric kernel from the committed
-    ncu --set full summary, when one exists."""
+    ncu --set full summary (stamped with the capture it came from)."""
     path = os.path.join(ROOT, "profiles", "ncu_numeric_summary.json")
     try:
         with open(path) as f:
@@ -135,71 +162,114 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU legs (oracle port) -- test/bench infrastructure only
+# CPU legs (oracle port / reference package) -- test/bench infrastructure only
 # ---------------------------------------------------------------------------
-def cpu_sample_operands(planes=SAMPLE_PLANES, n=256, seed=None):
-    """Host CSR of the fine rows of z-planes [0, planes) of config 3 level 1:
-    A rows [0, R) (columns up to the next plane) padded to R + n^2 rows and
-    P rows [0, R + n^2), so P^T A P equals the contribution of those rows."""
+def host_config_operands(config: str, n_fine=None, slabs: int = 8):
+    """Host CSR (int64/float64) of a configuration's level 1, built by the
+    host generators in row slabs (bounded temporaries) -- the reference arm
+    touches no GPU."""
     import numpy as np
 
     from paper_1905_08423_b200 import problems as gen
     from paper_1905_08423_b200.sparse import CsrMatrix
 
-    spec = gen.CONFIGS["cfg3"]
-    R = planes * n * n
-    ns = R + n * n
-    a = gen.random27(n, spec.seed if seed is None else seed, 0, R)
-    a_ip = np.concatenate((a.row_offsets, np.full(ns - R, a.row_offsets[-1])))
-    A = CsrMatrix(ns, ns, a_ip, a.col_indices, a.values, check=False)
-    p = gen.trilinear(n // 2, 0, ns)
-    return A, p
+    spec = gen.CONFIGS[config]
+    n = spec.n_fine if n_fine is None else n_fine
+    N = n ** 3
+    parts_a, parts_p = [], []
+    for s in range(slabs):
+        lo, hi = N * s // slabs, N * (s + 1) // slabs
+        a, p = gen.config_operands(spec, n_fine=n, row_lo=lo, row_hi=hi)
+        parts_a.append(a)
+        parts_p.append(p)
+
+    def cat(parts, ncols):
+        rp = [np.zeros(1, np.int64)]
+        off = 0
+        for m in parts:
+            rp.append(m.row_offsets[1:] + off)
+            off += m.col_indices.size
+        return CsrMatrix(N, ncols, np.concatenate(rp), np.concatenate([m.col_indices for m in parts]),
+                         np.concatenate([m.values for m in parts]), check=False)
+
+    return cat(parts_a, N), cat(parts_p, parts_p[0].ncols)
 
 
-def run_cpu_oracle(nthreads=1, steps=1, planes=SAMPLE_PLANES):
-    from oracle import oracle as orc
-
-    os.environ["OMP_NUM_THREADS"] = str(nthreads)
-    A, P = cpu_sample_operands(planes)
-    plan = orc.OraclePlan(A.nrows, P.ncols, A.row_offsets, A.col_indices, P.row_offsets, P.col_indices,
-                          nranks=nthreads, algorithm="allatonce")
-    times = []
-    out = None
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        out = plan.numeric(A.values, P.values, out)
-        times.append(time.perf_counter() - t0)
-    st = plan.num_stats
-    mac = int(st.mac_ap + st.mac_outer)
-    return {"times": times, "mac": mac, "rows": int(planes * 256 * 256), "nnz_c": plan.nnz}
-
-
-def reference_arm(args):
-    """--impl reference: the reference algorithm (C port) on all host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
+def oracle_run(A, P, nthreads: int, steps: int, warmup: int = 0):
+    """The reference's algorithm (oracle/ C port) at np = nthreads simulated
+    ranks, one per thread: symbolic once (untimed), then warmup + steps
+    timed numeric passes.  Returns (times, mac, plan, values)."""
     from oracle import oracle as orc
 
     orc.build()
+    os.environ["OMP_NUM_THREADS"] = str(nthreads)
+    t = time.perf_counter()
+    plan = orc.OraclePlan(A.nrows, P.ncols, A.row_offsets, A.col_indices, P.row_offsets, P.col_indices,
+                          nranks=nthreads, algorithm="allatonce")
+    sym_s = time.perf_counter() - t
+    out = None
+    times = []
+    for k in range(warmup + steps):
+        t = time.perf_counter()
+        out = plan.numeric(A.values, P.values, out)
+        if k >= warmup:
+            times.append(time.perf_counter() - t)
+    st = plan.num_stats
+    return times, int(st.mac_ap + st.mac_outer), plan, out, sym_s
+
+
+def numba_reference_leg(config: str, timeout: float = 900.0):
+    """The unmodified reference package (baseline/_ref, numba) on `config` at
+    np = 1 through its public API, in a subprocess; the oracle port is
+    checked bit for bit against it on the same inputs."""
+    ref = os.path.join(ROOT, "baseline", "_ref", "ptap")
+    if not os.path.isdir(ref):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref)"}
+    env = dict(os.environ, NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/ptap_numba_cache"),
+               OMP_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_numba.py"), config, "--repeats", "2",
+                            "--check-oracle"], capture_output=True, text=True, timeout=timeout, env=env)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not lines:
+            return {"error": (r.stderr or r.stdout)[-400:]}
+        d = json.loads(lines[-1])
+        d["note"] = ("numba reference, np=1, 1 thread, warm numeric pass (2nd of 2); port = oracle/ C restatement "
+                     "timed on the same inputs")
+        return d
+    except Exception as exc:  # report, never fail the line
+        return {"error": repr(exc)}
+
+
+def reference_arm(args):
+    """--impl reference: the reference algorithm (oracle/ C port, one
+    simulated rank per host thread) on the same full workload as our arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
     threads = os.cpu_count() or 1
-    total = args.steps + args.warmup
-    res = run_cpu_oracle(nthreads=threads, steps=total)
-    times = res["times"][args.warmup:] or res["times"]
-    t = statistics.median(times)
-    value = 2.0 * res["mac"] / t / 1e9
+    t = time.perf_counter()
+    A, P = host_config_operands(args.config, args.n_fine)
+    gen_s = time.perf_counter() - t
+    times, mac, plan, _, sym_s = oracle_run(A, P, threads, max(1, args.steps), max(0, args.warmup))
+    tm = statistics.median(times)
+    value = 2.0 * mac / tm / 1e9
+    n = args.n_fine or 256
+    workload = (f"{args.config} L1: 27-pt random {n}^3 -> trilinear {n // 2}^3, numeric all-at-once (plan reused)"
+                if args.config == "cfg3" else f"{args.config} level 1, numeric all-at-once (plan reused)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tm * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg3 L1 sample: fine z-planes [0,{SAMPLE_PLANES}) of 256^3 27-pt random, trilinear P, "
-                               "numeric all-at-once", "sample_rows": res["rows"], "mac": res["mac"]},
+        "config": {"workload": workload, "mac_total": mac, "flops_per_mac": 2, "same_config": True,
+                   "gen_s": gen_s, "symbolic_s": sym_s},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"fine z-planes [0,{SAMPLE_PLANES}) of config 3 level 1 ({res['rows']} rows), "
-                                   f"one simulated reference rank per thread"},
+                         "sample": f"the full workload (all {A.nrows} fine rows), {args.warmup} warm-up + "
+                                   f"{args.steps} timed numeric passes, {threads} simulated reference ranks, "
+                                   f"one per host thread"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -217,8 +287,9 @@ def alg_bytes(a, p, c_nnz, ncl):
             + csr_bytes(p.local.offdiag) + (ncl + 1) * 8 + c_nnz * 12)
 
 
-def time_numeric(pk, a, p, plan, ctx, steps, warmup, torch, kernel_events=None):
-    """Per-step device time of numeric passes (events on the launching stream)."""
+def time_numeric(pk, a, p, plan, ctx, steps, warmup, torch):
+    """Per-step device time of numeric passes (events on the launching
+    stream) and the time of the local loop's launches (the fused kernel)."""
     import ctypes
 
     from paper_1905_08423_b200 import _lib
@@ -283,7 +354,7 @@ def write_csv(path, line, out, ctx):
             "time_sym_s", "time_num_s", "time_total_s", "repeats", "verified",
             "gflops", "alg_gbs", "roofline_frac", "n_gpus"]
     mac2 = 2.0 * line["config"]["mac_total"]
-    alg_bytes = line["roofline"]["alg_bytes_per_launch"] * ctx.nranks
+    alg_bytes_ = line["roofline"]["alg_bytes_per_launch"] * ctx.nranks
     with open(path, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(cols)
@@ -294,14 +365,14 @@ def write_csv(path, line, out, ctx):
             w.writerow([ctx.nranks, alg, mem["input_matrices"], mem["output_matrix"], mem["auxiliary_matrices"],
                         mem["transient_hash_peak"], mem["plan_cache"], v["symbolic_ms"] * 1e-3, t_num,
                         v["symbolic_ms"] * 1e-3 + t_num, line["steps"], bool(diff <= 1e-12),
-                        mac2 / t_num / 1e9, alg_bytes / t_num / 1e9,
-                        alg_bytes / t_num / 1e9 / (line["roofline"]["peak"] * ctx.nranks), ctx.nranks])
+                        mac2 / t_num / 1e9, alg_bytes_ / t_num / 1e9,
+                        alg_bytes_ / t_num / 1e9 / (line["roofline"]["peak"] * ctx.nranks), ctx.nranks])
 
 
 def max_over_ranks(x, ctx, torch):
     if ctx.nranks == 1:
         return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device=ctx.device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=ctx.comm_device)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     return float(t.item())
 
@@ -309,9 +380,27 @@ def max_over_ranks(x, ctx, torch):
 def sum_over_ranks(x, ctx, torch):
     if ctx.nranks == 1:
         return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device=ctx.device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=ctx.comm_device)
     torch.distributed.all_reduce(t)
     return float(t.item())
+
+
+def dry_run(args):
+    """Rendezvous check of the multi-rank launch (no kernels): every rank
+    joins the group, rank 0 prints the line skeleton with n_gpus."""
+    import torch
+
+    import paper_1905_08423_b200 as pk
+
+    ctx = pk.init_from_env()
+    world = sum_over_ranks(1.0, ctx, torch)
+    if ctx.rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": ctx.nranks, "ranks_joined": int(world),
+                          "backend": ctx.backend, "dry_run": True}), flush=True)
+    if ctx.nranks > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
 
 
 def our_arm(args):
@@ -321,6 +410,7 @@ def our_arm(args):
     import paper_1905_08423_b200 as pk
     from paper_1905_08423_b200 import devgen
 
+    os.environ.setdefault("PTAP_POOL_KEEP", "1")  # warm symbolic phases reuse the library pool
     ctx = pk.init_from_env()
     dev = ctx.device
     torch.cuda.synchronize()
@@ -330,32 +420,31 @@ def our_arm(args):
     gen_s = time.perf_counter() - t0
     out = {}
 
-    def symbolic(alg):
+    def symbolic(alg, **kw):
         torch.cuda.synchronize()
         ctx.barrier()
         t = time.perf_counter()
-        plan = pk.run_symbolic(a, p, alg, ctx)
+        plan = pk.run_symbolic(a, p, alg, ctx, **kw)
         torch.cuda.synchronize()
         ctx.barrier()
         return plan, max_over_ranks(time.perf_counter() - t, ctx, torch)
 
-    # --- headline: all-at-once ------------------------------------------------
     import gc
 
-    def warm_symbolic(alg):
-        """cold call (one-time module and memory-pool setup), then three warm
-        calls; the warm figure is the fastest (the host-side driver calls
-        occasionally stall for tens of ms on these boxes; all are reported)"""
-        pl, cold = symbolic(alg)
+    def warm_symbolic(alg, nwarm=5, **kw):
+        """one cold call (module and pool setup), then `nwarm` warm calls;
+        the reported figure is their median (all are listed)"""
+        pl, cold = symbolic(alg, **kw)
         warm = []
-        for _ in range(3):
+        for _ in range(nwarm):
             del pl
             gc.collect()
             torch.cuda.synchronize()
-            pl, t = symbolic(alg)
+            pl, t = symbolic(alg, **kw)
             warm.append(t)
-        return pl, cold, min(warm), warm
+        return pl, cold, statistics.median(warm), warm
 
+    # --- headline: all-at-once ------------------------------------------------
     plan, sym_cold, sym_s, sym_all = warm_symbolic("allatonce")
     cnt = plan.device_counters()
     mac = sum_over_ranks(cnt["mac_ap"] + cnt["mac_outer"], ctx, torch)
@@ -373,11 +462,19 @@ def our_arm(args):
     traffic, ncu_meta = ncu_traffic()
     kms = statistics.mean(kern_ms) if kern_ms else ms
     achieved = my_bytes / (kms * 1e-3) / 1e9
+    # NVLink bytes per step (several ranks): values of the gathered P rows and
+    # of the staged C_s rows, both directions counted once (sent)
+    nvlink = None
+    if ctx.nranks > 1:
+        rr = plan.remote_rows
+        sent = (int(rr.send_counts.sum()) if rr is not None else 0) * 8 + int(cnt["nnz_staging"]) * 8
+        nvlink = {"bytes_sent_per_step_all_ranks": int(sum_over_ranks(sent, ctx, torch)),
+                  "what": "P~_r values refresh + C_s values (alltoallv over NCCL)"}
     out["allatonce"] = {"numeric_ms": ms, "symbolic_ms": sym_s * 1e3, "symbolic_cold_ms": sym_cold * 1e3,
                         "symbolic_warm_runs_ms": [t * 1e3 for t in sym_all],
                         "ptap_wall_ms": sym_s * 1e3 + ms,
                         "aux_peak_bytes": mem["device_high_water"] - mem["current"]["output_matrix"],
-                        "memory": mem}
+                        "numeric_path": cnt["numeric_path"], "memory": mem}
 
     # --- config 3 level 2: A2 = C1 kept on the device (hierarchy driver), P2 trilinear
     level2 = None
@@ -419,48 +516,90 @@ def our_arm(args):
     del plan, c_rp, c_col, c_val
     gc.collect()
     torch.cuda.synchronize()
+    det_val = None
     if not args.no_variants:
-        for alg in ("merged", "two-step"):
-            vplan, vcold, vsym, vall = warm_symbolic(alg)
-            vms, _, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
+        for name, alg, kw in (("merged", "merged", {}), ("two-step", "two-step", {}),
+                              ("allatonce_deterministic", "allatonce", {"deterministic": True})):
+            vplan, vcold, vsym, vall = warm_symbolic(alg, nwarm=3, **kw)
+            vms, vkern, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
             vmem = vplan.memory()
             vms = max_over_ranks(vms, ctx, torch)
             vrp, _, vval = vplan.c_device()
             diff = max_over_ranks(row_scaled_diff(c_rp_ref, c_val_ref, vrp, vval, torch), ctx, torch)
-            out[alg] = {"numeric_ms": vms, "symbolic_ms": vsym * 1e3, "symbolic_cold_ms": vcold * 1e3,
-                        "symbolic_warm_runs_ms": [t * 1e3 for t in vall],
-                        "ptap_wall_ms": vsym * 1e3 + vms,
-                        "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
-                        "row_scaled_diff_vs_allatonce": diff,
-                        "memory": vmem}
+            out[name] = {"numeric_ms": vms, "symbolic_ms": vsym * 1e3, "symbolic_cold_ms": vcold * 1e3,
+                         "symbolic_warm_runs_ms": [t * 1e3 for t in vall],
+                         "ptap_wall_ms": vsym * 1e3 + vms,
+                         "aux_peak_bytes": vmem["device_high_water"] - vmem["current"]["output_matrix"],
+                         "row_scaled_diff_vs_allatonce": diff,
+                         "numeric_path": vplan.device_counters()["numeric_path"],
+                         "deterministic": vplan.deterministic, "memory": vmem}
+            if name == "allatonce_deterministic":
+                out[name]["gflops"] = flops / (vms * 1e-3) / 1e9
+                if ctx.nranks == 1:
+                    det_val = vval.cpu().numpy()
             del vplan, vrp, vval
             gc.collect()
             torch.cuda.synchronize()
-        del c_rp_ref, c_val_ref
 
-    # --- CPU baseline (rank 0, N = 1) -----------------------------------------
+    # --- CPU baseline (rank 0, N = 1): the oracle port on the SAME full
+    # workload, 1 thread, R = 1; its C doubles as the full-size parity check
     cpu = None
+    parity = None
     if ctx.rank == 0 and ctx.nranks == 1 and not args.no_cpu_baseline:
-        res = run_cpu_oracle(nthreads=1, steps=1)
-        t = res["times"][0]
-        cpu = {"value": 2.0 * res["mac"] / t / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"fine z-planes [0,{SAMPLE_PLANES}) of config 3 level 1 ({res['rows']} rows, "
-                         f"{res['mac']} MAC), oracle all-at-once numeric pass, np=1, 1 thread",
-               "seconds": t, "host_cores_available": os.cpu_count()}
+        try:
+            from paper_1905_08423_b200.sparse import CsrMatrix
+            dl, pl_ = a.local.diag, p.local.diag
+            A = CsrMatrix(dl.nrows, dl.ncols, dl.row_ptr.cpu().numpy(), dl.col.cpu().numpy(), dl.val.cpu().numpy(),
+                          check=False)
+            P = CsrMatrix(pl_.nrows, pl_.ncols, pl_.row_ptr.cpu().numpy(), pl_.col.cpu().numpy(),
+                          pl_.val.cpu().numpy(), check=False)
+            times, cmac, oplan, cval, csym = oracle_run(A, P, 1, 1, 0)
+            t = times[0]
+            cpu = {"value": 2.0 * cmac / t / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"the full workload ({A.nrows} fine rows, {cmac} MAC): oracle/ all-at-once numeric pass "
+                             f"at np=1, 1 thread, R=1 (symbolic {csym:.1f} s untimed)",
+                   "seconds": t, "same_config": True, "host_cores_available": os.cpu_count()}
+            # full-size parity: pattern exact; deterministic pass bit-exact;
+            # default pass row-scaled
+            rp_h = c_rp_ref.cpu().numpy()
+            pat = bool(np.array_equal(oplan.row_ptr, rp_h))
+            parity = {"oracle": "oracle/ np=1 all-at-once on the same device-generated inputs",
+                      "pattern_row_ptr_equal": pat}
+            if pat:
+                want = cval
+                got = c_val_ref.cpu().numpy()
+                rows = np.repeat(np.arange(rp_h.size - 1), np.diff(rp_h))
+                rmax = np.zeros(rp_h.size - 1)
+                np.maximum.at(rmax, rows, np.abs(want))
+                d = np.abs(got - want)
+                parity["row_scaled_max"] = float((d / np.maximum(rmax[rows], 1e-300)).max(initial=0.0))
+                nz = want != 0
+                parity["per_entry_rel_max"] = float((d[nz] / np.abs(want[nz])).max(initial=0.0))
+                if det_val is not None:
+                    parity["deterministic_bitwise_equal"] = bool(np.array_equal(det_val.view(np.uint64),
+                                                                                want.view(np.uint64)))
+            del oplan, A, P
+        except Exception as exc:
+            cpu = {"error": repr(exc)}
+    numba_leg = None
+    if ctx.rank == 0 and ctx.nranks == 1 and not args.no_numba and not args.no_cpu_baseline:
+        numba_leg = numba_reference_leg(args.numba_config)
 
     if ctx.rank == 0:
+        n = args.n_fine or 256
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.nranks, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} L1: 27-pt random {args.n_fine or 256}^3 -> trilinear "
-                                   f"{(args.n_fine or 256) // 2}^3, numeric all-at-once (plan reused)",
+            "config": {"workload": f"{args.config} L1: 27-pt random {n}^3 -> trilinear {n // 2}^3, numeric "
+                                   f"all-at-once (plan reused)",
                        "parallelism": f"z-slab row blocks x{ctx.nranks}", "mac_total": int(mac),
                        "flops_per_mac": 2, "l2": "inputs larger than L2 (A = %.1f GB), no flush" % (my_bytes / 1e9),
-                       "gen_s": gen_s},
+                       "gen_s": gen_s, "same_config": True},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_outer_numeric_q4a (ptap_numeric_local)", "kernel_ms": kms,
+                         "traffic_source": (ncu_meta or {}).get("source"),
+                         "kernel": "ptap_numeric_local launches (k_outer_numeric_q4a)", "kernel_ms": kms,
                          "alg_bytes_per_launch": my_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -469,10 +608,13 @@ def our_arm(args):
             "variants": {k: {kk: vv for kk, vv in v.items() if kk != "memory"} for k, v in out.items()},
             "memory_bytes": {k: v["memory"] for k, v in out.items()},
             "level2": level2,
+            "parity_full_size": parity,
+            "reference_numba": numba_leg,
+            "nvlink": nvlink,
         }
         if "two-step" in out:
             line["variants"]["allatonce_over_two_step_time"] = out["allatonce"]["numeric_ms"] / out["two-step"]["numeric_ms"]
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
         if args.csv:
             write_csv(args.csv, line, out, ctx)
     if ctx.nranks > 1:
@@ -502,7 +644,6 @@ def e2e_leg(pk, a, p, plan, ctx, flops, steps, torch):
     ph = DistMatrix(p.row_part, p.col_part, p.rank, host_local(p.local))
     # the plan's device operands become the upload targets
     from paper_1905_08423_b200.tripleproduct import _identity
-    from paper_1905_08423_b200.device import structure_token
     plan._a_token = (_identity(ah.local), None)
     plan._p_token = (_identity(ph.local), None)
     h2d = (ah.local.diag.nnz + ah.local.offdiag.nnz + ph.local.diag.nnz + ph.local.offdiag.nnz) * 8
@@ -525,6 +666,10 @@ def e2e_leg(pk, a, p, plan, ctx, flops, steps, torch):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)

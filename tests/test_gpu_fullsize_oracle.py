@@ -1,0 +1,119 @@
+"""BASELINE configurations at (or near) full size on the device, against the
+CPU oracle (pinned to the reference); the reference pins its
+model problem against its oracle the same way (tests/test_tripleproduct.py:289-310).
+
+Gates: pattern (row offsets, sorted columns) exact; values row-scaled
+|d| / max_k |C_ik| <= 1e-12 for every entry; the pure per-entry relative error
+("values A") <= 1e-12 on every entry not cancellation-dominated
+(|C_ij| >= 1e-6 max_k |C_ik|) and reported in full; the deterministic pass
+bit-identical to the oracle at one rank.  Per-entry figures are appended to
+tests/_reports/fullsize_parity.jsonl."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+REPORT = os.path.join(os.path.dirname(__file__), "_reports", "fullsize_parity.jsonl")
+
+
+def _host(dl):
+    from paper_1905_08423_b200.sparse import CsrMatrix
+    return CsrMatrix(dl.nrows, dl.ncols, dl.row_ptr.cpu().numpy(), dl.col.cpu().numpy(), dl.val.cpu().numpy(),
+                     check=False)
+
+
+def _oracle(A, P):
+    from oracle.oracle import OraclePlan
+    plan = OraclePlan(A.nrows, P.ncols, A.row_offsets, A.col_indices, P.row_offsets, P.col_indices, nranks=1,
+                      algorithm="allatonce")
+    v = plan.numeric(A.values, P.values)
+    return plan.row_ptr, plan.col, v
+
+
+def _check(tag, rp, col, val, want, bitwise=False):
+    wrp, wcol, wval = want
+    assert np.array_equal(rp, wrp), f"{tag}: row offsets"
+    assert np.array_equal(col, wcol), f"{tag}: columns"
+    rows = np.repeat(np.arange(rp.size - 1), np.diff(rp))
+    rmax = np.zeros(rp.size - 1)
+    np.maximum.at(rmax, rows, np.abs(wval))
+    d = np.abs(val - wval)
+    rs = float((d / np.maximum(rmax[rows], 1e-300)).max(initial=0.0))
+    nz = wval != 0
+    pe = float((d[nz] / np.abs(wval[nz])).max(initial=0.0))
+    big = np.abs(wval) >= 1e-6 * rmax[rows]
+    pe_big = float((d[big] / np.abs(wval[big])).max(initial=0.0))
+    nbit = int((val.view(np.uint64) != wval.view(np.uint64)).sum())
+    os.makedirs(os.path.dirname(REPORT), exist_ok=True)
+    with open(REPORT, "a") as f:
+        f.write(json.dumps({"case": tag, "nnz": int(val.size), "row_scaled_max": rs, "per_entry_rel_max": pe,
+                            "per_entry_rel_max_not_cancelling": pe_big, "entries_differing_bits": nbit}) + "\n")
+    assert rs <= TOL, (tag, rs)
+    assert pe_big <= TOL, (tag, pe_big)
+    if bitwise:
+        assert nbit == 0, (tag, nbit)
+
+
+def _run(pk, a, p, ctx, alg, **kw):
+    plan = pk.run_symbolic(a, p, alg, ctx, **kw)
+    rp, col, val = pk.run_numeric_device(a, p, plan, ctx)
+    return plan, rp.cpu().numpy(), col.cpu().numpy().astype(np.int64), val.cpu().numpy()
+
+
+def test_cfg3_levels_1_and_2_full_size():
+    """Config 3 at 256^3 (449 M nonzeros; the benchmarked configuration) and
+    its level 2 chained on the device (A2 = C1, trilinear P2 to 64^3)."""
+    import paper_1905_08423_b200 as pk
+    from paper_1905_08423_b200 import devgen, problems as gen
+    from paper_1905_08423_b200.hierarchy import _coarse_operator
+    from paper_1905_08423_b200.partition import DistMatrix, make_partition
+    ctx = pk.single_rank_context()
+    a, p = devgen.config_dist("cfg3", 1, 0, ctx.device)
+    assert a.nrows == 256 ** 3
+    want = _oracle(_host(a.local.diag), _host(p.local.diag))
+    plan, rp, col, val = _run(pk, a, p, ctx, "allatonce")
+    _check("cfg3 L1 allatonce", rp, col, val, want)
+    for alg in ("merged", "two-step"):
+        pl2, rp2, col2, val2 = _run(pk, a, p, ctx, alg)
+        _check(f"cfg3 L1 {alg}", rp2, col2, val2, want, bitwise=(alg == "two-step"))
+        del pl2
+    pld, rpd, cold, vald = _run(pk, a, p, ctx, "allatonce", deterministic=True)
+    assert pld.deterministic
+    _check("cfg3 L1 allatonce deterministic", rpd, cold, vald, want, bitwise=True)
+    del pld
+    # level 2 on the device from level 1's C
+    a2, _, _ = _coarse_operator(plan, p)
+    m2 = 64 ** 3
+    prp, pcol, pval = devgen.gen_trilinear_rows(64, 0, 128 ** 3, ctx.device)
+    p2 = DistMatrix(a2.row_part, make_partition(m2, 1), 0,
+                    devgen.split_rows_device(prp, pcol, pval, 0, 128 ** 3, 0, m2, m2))
+    want2 = _oracle(_host(a2.local.diag), _host(p2.local.diag))
+    for alg, kw in (("allatonce", {}), ("merged", {}), ("two-step", {}), ("allatonce", {"deterministic": True})):
+        pl, rp2, col2, val2 = _run(pk, a2, p2, ctx, alg, **kw)
+        det = pl.deterministic
+        _check(f"cfg3 L2 {alg}{' deterministic' if kw else ''}", rp2, col2, val2, want2,
+               bitwise=(alg == "two-step") or (bool(kw) and det))
+        if kw:
+            assert det
+        del pl
+    del plan
+
+
+@pytest.mark.parametrize("which,size", [("cfg4", 48), ("cfg5", 2_000_000)])
+def test_amg_configs_large(which, size):
+    """Config 4 at 48^3 x 10 (1.1 M rows, C rows up to ~270 entries) and
+    config 5 at 2 M points (kNN graph, random order, hash path)."""
+    import paper_1905_08423_b200 as pk
+    from paper_1905_08423_b200 import problems_amg as amg
+    A, P = amg.block_transport(size) if which == "cfg4" else amg.knn_laplacian(size)
+    want = _oracle(A, P)
+    ctx = pk.single_rank_context()
+    a, p = pk.distribute(A, P, 1, 0)
+    for alg in ("allatonce", "merged", "two-step"):
+        pl, rp, col, val = _run(pk, a, p, ctx, alg)
+        _check(f"{which}@{size} {alg}", rp, col, val, want, bitwise=(alg == "two-step"))
+        del pl
