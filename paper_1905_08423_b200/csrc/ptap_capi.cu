@@ -923,6 +923,7 @@ ptap_status build_tile(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   const bool pstage = getenv("PTAP_TILE_PSTAGE") != nullptr;
   const int pvcap = pstage ? 3072 : 0;
   t.pstage = pstage ? 1 : 0;
+  t.a_evict_first = getenv("PTAP_TILE_NO_EVICT") ? 0 : 1;
   if (pstage)
     CK(launch_tile_pruns(nblk, n, op.ad_rp, op.ad_col, op.pd_rp, pnnz, pvcap, 1024, pr_n, pr_k, stats, st));
   else

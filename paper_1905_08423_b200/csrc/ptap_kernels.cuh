@@ -187,7 +187,8 @@ constexpr int TILE_MAXRUN = 16;    // runs of P rows staged per block
 struct TileArgs {
   int32_t nloc, nblk, nitems, ring_blocks, blkcap, grid;  // nitems = nblk + ownership delay
   int32_t napc;             // accumulator slots per row (>= widest AP row)
-  int32_t pstage;           // 1: stage the blocks' P runs in shared memory, 0: prefetch them into L1
+  int32_t pstage;           // 1: stage the blocks' P runs in shared memory
+  int32_t a_evict_first;    // 1: A's copies carry an L2 evict-first hint
   int32_t sm_aval, sm_acol, sm_pstage, sm_prp, sm_acc, sm_meta, sm_tail, sm_total;  // dynamic shared memory layout (bytes)
   const uint8_t *pr_n;      // [nblk] runs of P rows staged per block (0: read P from global memory)
   const int2 *pr_k;         // [nblk * TILE_MAXRUN] run [k0, k1) of P rows

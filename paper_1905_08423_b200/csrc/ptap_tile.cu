@@ -51,7 +51,10 @@ namespace ptapdev {
 namespace {
 
 constexpr int TW = 2;              // fold warps per CTA (even / odd rows of a block)
-constexpr int GW = 4;              // gather warps per CTA (run concurrently with the fold warps)
+#ifndef PTAP_TILE_GW
+#define PTAP_TILE_GW 2
+#endif
+constexpr int GW = PTAP_TILE_GW;   // gather warps per CTA (run concurrently with the fold warps)
 constexpr int NT = (TW + GW) * 32;
 constexpr int TR = TILE_ROWS;      // rows per block (item)
 constexpr int AST = 33;            // accumulator stride per slot (doubles): conflict-free both ways
@@ -90,6 +93,16 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// the same with an L2 eviction-priority hint: A is streamed once, so its
+// lines go first and leave L2 to P's rows and the AP ring
+__device__ __forceinline__ void tma_bulk_g2s_stream(void *dst, const void *src, uint32_t bytes,
+                                                    unsigned long long *bar) {
+  asm volatile(
+      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -166,8 +179,13 @@ __device__ __forceinline__ void stage_block(const Ops &op, const TileArgs &ta, i
     fence_proxy_async();
     mbar_arrive_expect_tx(&T.bar,
                           (uint32_t)((cend - c0) * 4 + (vend - v0) * 8 + (int64_t)ptot * 8 + (int64_t)rtot * 8));
-    if (cend > c0) tma_bulk_g2s(acol, op.ad_col + c0, (uint32_t)((cend - c0) * 4), &T.bar);
-    if (vend > v0) tma_bulk_g2s(aval, op.ad_val + v0, (uint32_t)((vend - v0) * 8), &T.bar);
+    if (ta.a_evict_first) {
+      if (cend > c0) tma_bulk_g2s_stream(acol, op.ad_col + c0, (uint32_t)((cend - c0) * 4), &T.bar);
+      if (vend > v0) tma_bulk_g2s_stream(aval, op.ad_val + v0, (uint32_t)((vend - v0) * 8), &T.bar);
+    } else {
+      if (cend > c0) tma_bulk_g2s(acol, op.ad_col + c0, (uint32_t)((cend - c0) * 4), &T.bar);
+      if (vend > v0) tma_bulk_g2s(aval, op.ad_val + v0, (uint32_t)((vend - v0) * 8), &T.bar);
+    }
   }
   __syncwarp();
   if (lane < nrun) {
@@ -188,7 +206,7 @@ __device__ __forceinline__ void stage_block(const Ops &op, const TileArgs &ta, i
 // ---------------------------------------------------------------------------
 // the numeric kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 4) k_tile_numeric(Ops op, MapArgs mp, TileArgs ta, const int64_t *c_rp,
+__global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric(Ops op, MapArgs mp, TileArgs ta, const int64_t *c_rp,
                                                           double *c_val, int blk_lo, int blk_hi, int item_hi) {
   extern __shared__ __align__(16) unsigned char tile_smem_raw[];
   double *aval = (double *)(tile_smem_raw + ta.sm_aval);
@@ -241,10 +259,10 @@ __global__ void __launch_bounds__(NT, 4) k_tile_numeric(Ops op, MapArgs mp, Tile
       const int tc = (int)(arow - c0), tv = (int)(arow - v0);
       const int maxlen = (ta.dbg & 8) ? 0 : __reduce_max_sync(FULL, len);
       int run = 0, r = 0;
-      // entry e's A value, P row (offset into pbase), length, values and slot bytes
-      double na = 0.0, npv[8];
-      uint32_t nsb[8];
+      // entry e's A value, P row (offset into pbase) and length; the next
+      // entry's are loaded while this one's updates run
       int nps = 0, npl = 0;
+      double na = 0.0;
       auto fetch = [&](int e) {
         npl = 0;
         if (e < len) {
@@ -262,46 +280,36 @@ __global__ void __launch_bounds__(NT, 4) k_tile_numeric(Ops op, MapArgs mp, Tile
             nps = pk0;
           }
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const bool act = u < npl;
-          npv[u] = act ? pbase[nps + u] : 0.0;
-          nsb[u] = ldg_u8_or(act, smp + run + u, 0u);
-        }
       };
       fetch(0);
 #pragma unroll 1
       for (int e = 0; e < maxlen; ++e) {
         const double ae = na;
         const int pse = nps, ple = npl;
-        double pv[8];
-        uint32_t sb[8];
+        fetch(e + 1);
+        const int maxpl = __reduce_max_sync(FULL, ple);
+#pragma unroll 1
+        for (int u0 = 0; u0 < maxpl; u0 += 4) {
+          double pv[4], old[4];
+          uint32_t sb[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          pv[u] = npv[u];
-          sb[u] = nsb[u];
+          for (int q = 0; q < 4; ++q) {
+            const bool act = u0 + q < ple;
+            pv[q] = act ? pbase[pse + u0 + q] : 0.0;
+            sb[q] = ldg_u8_or(act, smp + run + u0 + q, 0x80u);
+          }
+          // the slots of one entry's P row are distinct: load, then store
+#pragma unroll
+          for (int q = 0; q < 4; ++q) old[q] = (sb[q] & 0x80) ? 0.0 : acc[(sb[q] & 0x7f) * AST + lane];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (u0 + q < ple) {
+              const double prod = __dmul_rn(ae, pv[q]);
+              acc[(sb[q] & 0x7f) * AST + lane] = (sb[q] & 0x80) ? prod : __dadd_rn(old[q], prod);
+            }
+          }
         }
         run += ple;
-        fetch(e + 1);  // the next entry's loads are in flight during this one's updates
-        // the slots of one entry's P row are distinct: load, then store
-        double old[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) old[u] = (u < ple && !(sb[u] & 0x80)) ? acc[(sb[u] & 0x7f) * AST + lane] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (u < ple) {
-            const double prod = __dmul_rn(ae, pv[u]);
-            acc[(sb[u] & 0x7f) * AST + lane] = (sb[u] & 0x80) ? prod : __dadd_rn(old[u], prod);
-          }
-        }
-        if (__any_sync(FULL, ple > 8)) {  // P rows longer than 8 (rare): the rest one by one
-          for (int u = 8; u < ple; ++u) {
-            const uint32_t s2 = __ldg(smp + run - ple + u);
-            const double prod = __dmul_rn(ae, pbase[pse + u]);
-            double *ad = acc + (s2 & 0x7f) * AST + lane;
-            *ad = (s2 & 0x80) ? prod : __dadd_rn(*ad, prod);
-          }
-        }
       }
       __syncwarp();
       // ---- the ring slot must have been read by every reader of its previous
@@ -364,34 +372,52 @@ __global__ void __launch_bounds__(NT, 4) k_tile_numeric(Ops op, MapArgs mp, Tile
           const int w = (int)(c_rp[J + 1] - cb0);
           const uint8_t *qm = ta.qmap + ta.qmap_rp[J];
           // lane c owns positions c and c + 32 of C row J; contributors in
-          // ascending row order, 8 at a time: slot bytes, then AP values,
-          // then the sums
+          // ascending row order: slot bytes, then AP values, then the sums
           double acc0 = 0.0, acc1 = 0.0;
-          const bool two = w > 32;
+          if (w <= 32) {  // one position per lane, 16 contributors in flight
 #pragma unroll 1
-          for (int k0 = 0; k0 < nk; k0 += 8) {
-            uint32_t s0[8], s1[8];
+            for (int k0 = 0; k0 < nk; k0 += 16) {
+              uint32_t s0[16];
+              double v0[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int kk = k0 + u;
-              s0[u] = ldg_u8_or(kk < nk && lane < w, qm + kk * w + lane, 0xffu);
-              s1[u] = two ? ldg_u8_or(kk < nk && lane + 32 < w, qm + kk * w + lane + 32, 0xffu) : 0xffu;
+              for (int u = 0; u < 16; ++u) s0[u] = ldg_u8_or(k0 + u < nk && lane < w, qm + (k0 + u) * w + lane, 0xffu);
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int ab = g_apb[t0 + min(k0 + u, nk - 1)];
+                v0[u] = ld_cg_f64_if(s0[u] != 0xffu, ta.ring + ab + (s0[u] & 0xff));
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                // an absent entry adds pk * 0 = +-0: the running sum starts at
+                // +0 and a round-to-nearest sum of +0-started terms is never
+                // -0, so adding a signed zero leaves its bits unchanged
+                const double pk = (k0 + u < nk) ? g_pv[t0 + k0 + u] : 0.0;
+                acc0 = __dadd_rn(acc0, __dmul_rn(pk, v0[u]));
+              }
             }
-            double v0[8], v1[8];
+          } else {
+#pragma unroll 1
+            for (int k0 = 0; k0 < nk; k0 += 8) {
+              uint32_t s0[8], s1[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int ab = g_apb[t0 + min(k0 + u, nk - 1)];
-              v0[u] = ld_cg_f64_if(s0[u] != 0xffu, ta.ring + ab + (s0[u] & 0xff));
-              v1[u] = two ? ld_cg_f64_if(s1[u] != 0xffu, ta.ring + ab + (s1[u] & 0xff)) : 0.0;
-            }
+              for (int u = 0; u < 8; ++u) {
+                const int kk = k0 + u;
+                s0[u] = ldg_u8_or(kk < nk, qm + kk * w + lane, 0xffu);
+                s1[u] = ldg_u8_or(kk < nk && lane + 32 < w, qm + kk * w + lane + 32, 0xffu);
+              }
+              double v0[8], v1[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              // an absent entry adds pk * 0 = +-0: the running sum starts at
-              // +0 and a round-to-nearest sum of +0-started terms is never
-              // -0, so adding a signed zero leaves its bits unchanged
-              const double pk = (k0 + u < nk) ? g_pv[t0 + k0 + u] : 0.0;
-              acc0 = __dadd_rn(acc0, __dmul_rn(pk, v0[u]));
-              if (two) acc1 = __dadd_rn(acc1, __dmul_rn(pk, v1[u]));
+              for (int u = 0; u < 8; ++u) {
+                const int ab = g_apb[t0 + min(k0 + u, nk - 1)];
+                v0[u] = ld_cg_f64_if(s0[u] != 0xffu, ta.ring + ab + (s0[u] & 0xff));
+                v1[u] = ld_cg_f64_if(s1[u] != 0xffu, ta.ring + ab + (s1[u] & 0xff));
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const double pk = (k0 + u < nk) ? g_pv[t0 + k0 + u] : 0.0;
+                acc0 = __dadd_rn(acc0, __dmul_rn(pk, v0[u]));
+                acc1 = __dadd_rn(acc1, __dmul_rn(pk, v1[u]));
+              }
             }
           }
           if (lane < w) c_val[cb0 + lane] = acc0;
