@@ -194,6 +194,17 @@ ptap_status ptap_numeric_local_rows(ptap_plan *plan, const ptap_operands *ops, i
 ptap_status ptap_plan_c_last_row(ptap_plan *plan, const ptap_operands *ops, int32_t *last, void *stream);
 /* Synchronise and report device-side drift detected by the last numeric pass. */
 ptap_status ptap_plan_check(ptap_plan *plan, void *stream);
+/* Non-blocking variant: enqueue the copy of the pass's status word to pinned
+ * host memory (no host synchronisation; reports a failure of the PREVIOUS
+ * pass if one was pending), and read it later with ptap_plan_status_poll. */
+ptap_status ptap_plan_status_async(ptap_plan *plan, void *stream);
+ptap_status ptap_plan_status_poll(ptap_plan *plan);
+/* Owner side of the per-pass values-only refresh of the gathered P rows
+ * (update_remote_rows_numeric, src/comm.py:625-649): out[t] = value idx[t] of
+ * [P_d.val, P_o.val] (the symbolic gather's serve index), device buffers,
+ * asynchronous; an index past the structure flags drift in the plan status. */
+ptap_status ptap_pack_values(ptap_plan *plan, const ptap_operands *ops, const int64_t *idx, int64_t n,
+                             double *out, void *stream);
 /* Full structural check (reference verify_filled, src/spgemm.py:58-68, and the
  * CRC32 token of src/comm.py:517-524): digest of every structure array of the
  * operands against the symbolic-time digest; PTAP_ERR_DRIFT on mismatch.

@@ -75,6 +75,9 @@ _EXPORTS = {
     "ptap_numeric_local_rows": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), c_i64, c_i64, ctypes.c_int, c_p]),
     "ptap_plan_c_last_row": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), c_p, c_p]),
     "ptap_plan_check": (ctypes.c_int, [c_p, c_p]),
+    "ptap_plan_status_async": (ctypes.c_int, [c_p, c_p]),
+    "ptap_plan_status_poll": (ctypes.c_int, [c_p]),
+    "ptap_pack_values": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), c_p, c_i64, c_p, c_p]),
     "ptap_plan_verify": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), c_p]),
     "ptap_plan_get_ctilde": (ctypes.c_int, [c_p, ctypes.POINTER(CView)]),
     "ptap_plan_get_c": (ctypes.c_int, [c_p, ctypes.POINTER(CView)]),

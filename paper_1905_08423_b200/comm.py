@@ -70,16 +70,18 @@ class RankContext:
         torch.distributed.all_to_all_single(out, t, group=self.group)
         return out.cpu().numpy()
 
-    def alltoallv(self, send, send_counts, recv_counts, async_op=False):
+    def alltoallv(self, send, send_counts, recv_counts, async_op=False, out=None):
         """Flat alltoallv of one tensor: send[sum(send_counts)] grouped by
         destination, returns the flat receive buffer grouped by source
-        (ascending).  With async_op, returns (buffer, work handle)."""
+        (ascending).  With async_op, returns (buffer, work handle).  ``out``
+        (on the communication device) receives in place."""
         torch = _torch()
         sc = [int(x) for x in send_counts]
         rc = [int(x) for x in recv_counts]
         dev = self.comm_device
         src = send.to(dev) if send.device != dev else send
-        out = torch.empty(sum(rc), dtype=send.dtype, device=dev)
+        if out is None or out.device != dev or out.numel() != sum(rc):
+            out = torch.empty(sum(rc), dtype=send.dtype, device=dev)
         if self.nranks == 1:
             out.copy_(src)
             return (out, None) if async_op else out
@@ -218,17 +220,35 @@ def gather_remote_rows(ctx: RankContext, a_col_map: np.ndarray, p_row_part, p_lo
                       nbytes=int(rp.nbytes + cols_in.numel() * 4 + vals_in.numel() * 8 + src.numel() * 8))
 
 
-def refresh_remote_values(ctx: RankContext, rr: RemoteRows, p_local):
-    """Numeric values-only refresh of the gathered rows (src/comm.py:625-649)."""
+def refresh_remote_values(ctx: RankContext, rr: RemoteRows, p_local, plan_handle=None, ops=None):
+    """Numeric values-only refresh of the gathered rows (src/comm.py:625-649).
+
+    With the plan's handle the owner-side gather is one device kernel
+    (``ptap_pack_values``: the serve index into [P_d.val, P_o.val] read in
+    place, out-of-range indices flag drift in the plan status) and the
+    alltoallv receives straight into the gathered rows' value buffer: no
+    concatenation, no host synchronisation.  Without it (the standalone
+    SpGEMM) the same gather runs as a tensor index."""
     if ctx.nranks == 1:
         return
-    vcat = _p_values_concat(p_local)
-    if rr.serve_idx.numel() and int(rr.serve_idx.max().item()) >= vcat.numel():
-        raise StructuralDriftError("P changed structure since the symbolic gather")
-    vals = ctx.alltoallv(vcat[rr.serve_idx] if rr.serve_idx.numel() else vcat[:0], rr.send_counts, rr.recv_counts)
-    if vals.numel() != rr.val.numel():
-        raise StructuralDriftError("value update does not match the gathered structure")
-    rr.val.copy_(vals.to(rr.val.device))
+    torch = _torch()
+    n = rr.serve_idx.numel()
+    if plan_handle is not None:
+        from . import _lib
+        if getattr(rr, "send_buf", None) is None or rr.send_buf.numel() != n:
+            rr.send_buf = torch.empty(n, dtype=torch.float64, device=rr.serve_idx.device)
+        st = ops.struct()
+        stream = torch.cuda.current_stream().cuda_stream
+        _lib.check(_lib.load().ptap_pack_values(plan_handle, __import__("ctypes").byref(st),
+                                                rr.serve_idx.data_ptr() if n else None, n,
+                                                rr.send_buf.data_ptr() if n else None, stream), "pack values")
+        send = rr.send_buf
+    else:
+        vcat = _p_values_concat(p_local)
+        send = vcat[rr.serve_idx] if n else vcat[:0]
+    vals = ctx.alltoallv(send, rr.send_counts, rr.recv_counts, out=rr.val)
+    if vals.data_ptr() != rr.val.data_ptr():
+        rr.val.copy_(vals.to(rr.val.device), non_blocking=True)
 
 
 # ---------------------------------------------------------------------------

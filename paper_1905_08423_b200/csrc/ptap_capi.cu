@@ -100,6 +100,9 @@ struct ptap_plan {
   int64_t cur[5] = {0, 0, 0, 0, 0}, peak[5] = {0, 0, 0, 0, 0};
   int64_t prod_cur = 0, prod_peak = 0, total_cur = 0, total_peak = 0;
   int *d_status = nullptr;
+  int *h_status = nullptr;          // pinned: status of the last pass, copied asynchronously
+  cudaEvent_t status_ev = nullptr;
+  bool status_pending = false;
   unsigned long long *d_u64 = nullptr;  // 24 scratch counters
   bool released = false;
   bool symbolic_done = false;
@@ -1372,6 +1375,8 @@ ptap_status ptap_plan_destroy(ptap_plan *p) {
   cudaStreamSynchronize(0);
   cudaFree(p->d_status);
   cudaFree(p->d_u64);
+  if (p->h_status) cudaFreeHost(p->h_status);
+  if (p->status_ev) cudaEventDestroy(p->status_ev);
   delete p;
   // the last plan gone: give the pool's memory back to the driver (torch,
   // NCCL), unless PTAP_POOL_KEEP asks to keep it for the next plan
@@ -1738,6 +1743,52 @@ ptap_status ptap_numeric_merge(ptap_plan *p, const double *recv_vals, void *stre
     }
   }
   return PTAP_OK;
+}
+
+ptap_status ptap_pack_values(ptap_plan *p, const ptap_operands *ops, const int64_t *idx, int64_t n, double *out,
+                             void *stream) {
+  if (!p || !ops) return fail(PTAP_ERR_VALUE, "null argument");
+  if (n > 0 && (!idx || !out)) return fail(PTAP_ERR_VALUE, "null buffer");
+  CK(launch_pack_values(ops->p_diag.val, ops->p_diag.nnz, ops->p_off.val, ops->p_off.nnz, idx, n, out, p->d_status,
+                        (cudaStream_t)stream));
+  p->cnt.kernel_launches++;
+  return PTAP_OK;
+}
+
+// Non-blocking status: the device status word of this pass is copied to
+// pinned host memory behind the pass (and reset on the device); the result
+// is read by ptap_plan_status_poll, which waits only for that copy.
+ptap_status ptap_plan_status_async(ptap_plan *p, void *stream) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p->h_status) {
+    CK(cudaMallocHost(&p->h_status, sizeof(int)));
+    *p->h_status = 0;
+    CK(cudaEventCreateWithFlags(&p->status_ev, cudaEventDisableTiming));
+  }
+  if (p->status_pending) {  // fold the previous pass's status in first
+    CK(cudaEventSynchronize(p->status_ev));
+    const int prev = *p->h_status;
+    if (prev) {
+      p->status_pending = false;
+      return status_to_error(prev, "numeric");
+    }
+  }
+  CK(cudaMemcpyAsync(p->h_status, p->d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemsetAsync(p->d_status, 0, sizeof(int), st));
+  CK(cudaEventRecord(p->status_ev, st));
+  p->status_pending = true;
+  return PTAP_OK;
+}
+
+ptap_status ptap_plan_status_poll(ptap_plan *p) {
+  if (!p) return fail(PTAP_ERR_VALUE, "null plan");
+  if (!p->status_pending) return PTAP_OK;
+  CK(cudaEventSynchronize(p->status_ev));
+  p->status_pending = false;
+  const int s = *p->h_status;
+  *p->h_status = 0;
+  return status_to_error(s, "numeric");
 }
 
 ptap_status ptap_plan_check(ptap_plan *p, void *stream) {

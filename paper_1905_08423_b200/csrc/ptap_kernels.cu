@@ -1527,6 +1527,28 @@ cudaError_t launch_merge_slots(int64_t nrows, const int32_t *rows, const int64_t
   return cudaGetLastError();
 }
 
+// values-only refresh of the gathered P rows, owner side (reference
+// update_remote_rows_numeric with its gather_idx, src/comm.py:590-594,
+// 625-649): out[t] = value idx[t] of the concatenation [P_d.val, P_o.val],
+// read in place (no concatenated copy); an index past the structure sets
+// ST_DRIFT (the structure changed since the symbolic gather)
+__global__ void k_pack_values(const double *d_val, int64_t nd, const double *o_val, int64_t no, const int64_t *idx,
+                              int64_t n, double *out, int *status) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = idx[t];
+    double v = 0.0;
+    if (x >= 0 && x < nd) v = d_val[x];
+    else if (x >= nd && x < nd + no) v = o_val[x - nd];
+    else atomicOr(status, ST_DRIFT);
+    out[t] = v;
+  }
+}
+cudaError_t launch_pack_values(const double *d_val, int64_t nd, const double *o_val, int64_t no, const int64_t *idx,
+                               int64_t n, double *out, int *status, cudaStream_t st) {
+  if (n > 0) k_pack_values<<<nblk(n, 256), 256, 0, st>>>(d_val, nd, o_val, no, idx, n, out, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge_add(int64_t n, const int64_t *slot, const double *vals, double *c_val, cudaStream_t st) {
   if (n > 0) k_merge_add<<<nblk(n, 256), 256, 0, st>>>(n, slot, vals, c_val);
   return cudaGetLastError();

@@ -123,6 +123,8 @@ cudaError_t launch_merge_slots(int64_t nrows, const int32_t *rows, const int64_t
                                const int64_t *c_rp, const int32_t *c_col, int64_t *slot, int *status,
                                cudaStream_t st);
 cudaError_t launch_merge_add(int64_t n, const int64_t *slot, const double *vals, double *c_val, cudaStream_t st);
+cudaError_t launch_pack_values(const double *d_val, int64_t nd, const double *o_val, int64_t no, const int64_t *idx,
+                               int64_t n, double *out, int *status, cudaStream_t st);
 cudaError_t launch_count_cols(int64_t nnz, const int32_t *col, int64_t *cnt, cudaStream_t st);
 cudaError_t launch_transpose_scatter(int64_t nrows, const int64_t *rp, const int32_t *col, const int64_t *t_rp,
                                      int64_t *cursor, int32_t *t_row, int64_t *t_perm, cudaStream_t st);

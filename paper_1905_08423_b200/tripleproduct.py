@@ -246,8 +246,15 @@ class TripleProductPlan:
         self._c_alloc = AllocatedMatrix(local, nzd, nzo, np.ones(diag_idx.size, np.uint8), np.ones(off_idx.size, np.uint8),
                                         self)
 
+    def check(self):
+        """Wait for the status of the last numeric pass and raise on drift
+        (the device-result path reports it asynchronously)."""
+        if self._h:
+            _lib.check(self._lib().ptap_plan_status_poll(self._h), "numeric")
+
     def c_local(self) -> LocalMatrix:
         """Copy the current C values to the host LocalMatrix view."""
+        self.check()
         alloc = self.c_alloc
         _, _, val_d = self.c_device()
         diag_idx, off_idx = self._c_host
@@ -558,11 +565,11 @@ def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankCon
     L = _lib.load()
     with ctx.timer.phase("numeric"):
         _prepare(plan, a, p, ctx, symbolic=False)
-        if ctx.nranks > 1:
-            with ctx.timer.phase("gather"):
-                refresh_remote_values(ctx, plan.remote_rows, plan._p_dev)
         st = plan._ops.struct()
         stream = _stream_ptr()
+        if ctx.nranks > 1:
+            with ctx.timer.phase("gather"):
+                refresh_remote_values(ctx, plan.remote_rows, plan._p_dev, plan._h, plan._ops)
         _lib.check(L.ptap_numeric_send(plan._h, ctypes.byref(st), stream), "numeric send")
         work = recv_vals = None
         if ctx.nranks > 1:
@@ -575,10 +582,15 @@ def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankCon
             with ctx.timer.phase("exchange"):
                 if work is not None:
                     work.wait()
-            rv = recv_vals.to(ctx.device)
+            rv = recv_vals.to(ctx.device, non_blocking=True)
             _lib.check(L.ptap_numeric_merge(plan._h, ctypes.c_void_p(rv.data_ptr() if rv.numel() else 0), stream),
                        "numeric merge")
-        _lib.check(L.ptap_plan_check(plan._h, stream), "numeric")
+        if to_host:
+            _lib.check(L.ptap_plan_check(plan._h, stream), "numeric")
+        else:
+            # device result: the pass's status is copied behind it and read
+            # by the next call (or plan.check()) -- no host synchronisation
+            _lib.check(L.ptap_plan_status_async(plan._h, stream), "numeric")
     plan._sync_counters()
     return plan.c_local() if to_host else plan.c_device()
 
