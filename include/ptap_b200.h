@@ -196,7 +196,9 @@ ptap_status ptap_plan_c_last_row(ptap_plan *plan, const ptap_operands *ops, int3
 ptap_status ptap_plan_check(ptap_plan *plan, void *stream);
 /* Non-blocking variant: enqueue the copy of the pass's status word to pinned
  * host memory (no host synchronisation; reports a failure of the PREVIOUS
- * pass if one was pending), and read it later with ptap_plan_status_poll. */
+ * pass if one was pending), and read it later with ptap_plan_status_poll.
+ * Inside CUDA-graph capture the copy becomes part of the graph: synchronise
+ * after a replay, then poll. */
 ptap_status ptap_plan_status_async(ptap_plan *plan, void *stream);
 ptap_status ptap_plan_status_poll(ptap_plan *plan);
 /* Owner side of the per-pass values-only refresh of the gathered P rows

@@ -103,6 +103,7 @@ struct ptap_plan {
   int *h_status = nullptr;          // pinned: status of the last pass, copied asynchronously
   cudaEvent_t status_ev = nullptr;
   bool status_pending = false;
+  bool status_graph = false;        // a pass captured into a CUDA graph writes h_status on replay
   unsigned long long *d_u64 = nullptr;  // 24 scratch counters
   bool released = false;
   bool symbolic_done = false;
@@ -1776,6 +1777,14 @@ ptap_status ptap_plan_status_async(ptap_plan *p, void *stream) {
   }
   CK(cudaMemcpyAsync(p->h_status, p->d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemsetAsync(p->d_status, 0, sizeof(int), st));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    // captured: each replay writes the status to h_status; the caller
+    // synchronises before ptap_plan_status_poll reads it
+    p->status_graph = true;
+    return PTAP_OK;
+  }
   CK(cudaEventRecord(p->status_ev, st));
   p->status_pending = true;
   return PTAP_OK;
@@ -1783,7 +1792,14 @@ ptap_status ptap_plan_status_async(ptap_plan *p, void *stream) {
 
 ptap_status ptap_plan_status_poll(ptap_plan *p) {
   if (!p) return fail(PTAP_ERR_VALUE, "null plan");
-  if (!p->status_pending) return PTAP_OK;
+  if (!p->status_pending) {
+    if (p->status_graph && p->h_status) {  // replays of a captured pass (caller synchronised)
+      const int s = *p->h_status;
+      *p->h_status = 0;
+      return status_to_error(s, "numeric");
+    }
+    return PTAP_OK;
+  }
   CK(cudaEventSynchronize(p->status_ev));
   p->status_pending = false;
   const int s = *p->h_status;
