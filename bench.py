@@ -518,8 +518,12 @@ def our_arm(args):
     torch.cuda.synchronize()
     det_val = None
     if not args.no_variants:
+        # allatonce_hash: the same algorithm without plan maps (hash tables in
+        # every pass, nothing stored per row) -- the like-for-like comparator of
+        # two-step, which also probes hash tables every pass
         for name, alg, kw in (("merged", "merged", {}), ("two-step", "two-step", {}),
-                              ("allatonce_deterministic", "allatonce", {"deterministic": True})):
+                              ("allatonce_deterministic", "allatonce", {"deterministic": True}),
+                              ("allatonce_hash", "allatonce", {"maps": False})):
             vplan, vcold, vsym, vall = warm_symbolic(alg, nwarm=3, **kw)
             vms, vkern, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
             vmem = vplan.memory()
@@ -533,7 +537,7 @@ def our_arm(args):
                          "row_scaled_diff_vs_allatonce": diff,
                          "numeric_path": vplan.device_counters()["numeric_path"],
                          "deterministic": vplan.deterministic, "memory": vmem}
-            if name == "allatonce_deterministic":
+            if name in ("allatonce_deterministic", "allatonce_hash"):
                 out[name]["gflops"] = flops / (vms * 1e-3) / 1e9
                 if ctx.nranks == 1:
                     det_val = vval.cpu().numpy()
@@ -613,7 +617,13 @@ def our_arm(args):
             "nvlink": nvlink,
         }
         if "two-step" in out:
-            line["variants"]["allatonce_over_two_step_time"] = out["allatonce"]["numeric_ms"] / out["two-step"]["numeric_ms"]
+            ts = out["two-step"]["numeric_ms"]
+            line["variants"]["allatonce_over_two_step_time"] = out["allatonce"]["numeric_ms"] / ts
+            if "allatonce_hash" in out:
+                line["variants"]["allatonce_hash_over_two_step_time"] = out["allatonce_hash"]["numeric_ms"] / ts
+            if "allatonce_deterministic" in out:
+                line["variants"]["allatonce_deterministic_over_two_step_time"] = (
+                    out["allatonce_deterministic"]["numeric_ms"] / ts)
         print(json.dumps(line), flush=True)
         if args.csv:
             write_csv(args.csv, line, out, ctx)

@@ -158,7 +158,10 @@ ptap_status ptap_plan_destroy(ptap_plan *plan);
  *     bit-identical to the reference's summation order (src/tripleproduct.py:12-16,
  *     src/_kernels.py:446-515): the owner-computes kernel of ptap_tile.cu
  *     replaces the fp64-atomic scatter when the plan's local loop has
- *     one-rank structure (counters.numeric_path == 2 when it is in use). */
+ *     one-rank structure (counters.numeric_path == 2 when it is in use).
+ *   "maps" (-1/0/1): plan maps of the all-at-once / merged numeric pass:
+ *     -1 (default) kept when sampled rows repeat, 0 never (hash numeric path,
+ *     nothing stored per row), 1 always. */
 ptap_status ptap_plan_set_option(ptap_plan *plan, const char *key, int64_t value);
 
 /* Symbolic, phase 1: AP-row binning and the send-side structure C_s (all
@@ -229,6 +232,15 @@ ptap_status ptap_spgemm_ap_symbolic(const ptap_operands *ops, int64_t *nnz_out,
 ptap_status ptap_spgemm_ap_numeric(const ptap_operands *ops, const int64_t *row_ptr,
                                    const int32_t *col, double *val, void *stream);
 ptap_status ptap_device_free(void *ptr, void *stream);
+
+/* Transpose of a device CSR block with the value permutation (reference
+ * CsrMatrix.transpose_with_permutation, src/sparse.py:165-178): t_rp
+ * (ncols+1), t_col (nnz: source rows, ascending within each row), perm (nnz:
+ * t entry -> source entry, the stable argsort of the columns), t_val (nnz,
+ * optional: val[perm]).  Caller-owned device buffers.  Synchronises. */
+ptap_status ptap_transpose(int64_t nrows, int64_t ncols, const int64_t *row_ptr, const int32_t *col,
+                           const double *val, int64_t nnz, int64_t *t_row_ptr, int32_t *t_col, int64_t *perm,
+                           double *t_val, void *stream);
 
 /* Device generators of the BASELINE configurations (bit-identical to the
  * host generators in problems.py). Row block [row_lo, row_hi) of an n^3 grid.

@@ -88,6 +88,7 @@ _EXPORTS = {
                                                ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]),
     "ptap_spgemm_ap_numeric": (ctypes.c_int, [ctypes.POINTER(Operands), c_p, c_p, c_p, c_p]),
     "ptap_device_free": (ctypes.c_int, [c_p, c_p]),
+    "ptap_transpose": (ctypes.c_int, [c_i64, c_i64, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p]),
     "ptap_gen_stencil_rowptr": (ctypes.c_int, [ctypes.c_int, c_i64, c_i64, c_i64, c_p,
                                                ctypes.POINTER(c_i64), c_p]),
     "ptap_gen_stencil_fill": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, c_i64, c_i64,

@@ -122,6 +122,7 @@ struct ptap_plan {
   bool q4a = false;                 // identity bin 0 runs k_outer_numeric_q4a
   bool tile = false;                // ... and the deterministic owner-computes kernel replaces it
   bool deterministic = false;       // plan option: bitwise-repeatable numeric passes (tile kernel)
+  int maps_opt = -1;                // plan option: -1 row-sample policy, 0 no plan maps (hash path), 1 keep maps
   // symbolic-time image of the operands' structure (drift detection)
   int64_t img_shape[11] = {0};
   const void *img_ptr[11] = {nullptr};
@@ -719,7 +720,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   p->want_maps = false;
   Tracer tr;
   tr.on = tr.on && getenv("PTAP_TRACE")[0] == '2';
-  if (getenv("PTAP_NO_MAPS")) return PTAP_OK;
+  if (getenv("PTAP_NO_MAPS") || p->maps_opt == 0) return PTAP_OK;
   unsigned long long *mx = p->d_u64 + 12;
   CK(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), st));
   CK(launch_max_i64(p->nloc, p->ap_nnz, mx, st));      // AP row width  (slot byte)
@@ -736,7 +737,7 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   // operator whose rows do not repeat they would cost about as much memory as
   // the two-step's auxiliary matrices, so such a plan keeps no maps and
   // numeric runs the hash path (PTAP_MAPS=1 keeps them regardless)
-  if (!getenv("PTAP_MAPS") && p->rows_unstructured) return PTAP_OK;  // rows do not repeat: hash path
+  if (!getenv("PTAP_MAPS") && p->maps_opt != 1 && p->rows_unstructured) return PTAP_OK;  // rows do not repeat: hash path
   {
     // bin 0 through k_outer_numeric_q4: <= 128 map bytes per row and every
     // offset it touches within 32 bits
@@ -1395,6 +1396,10 @@ ptap_status ptap_plan_set_option(ptap_plan *p, const char *key, int64_t value) {
     p->deterministic = value != 0;
     return PTAP_OK;
   }
+  if (!strcmp(key, "maps")) {
+    p->maps_opt = value < 0 ? -1 : (value ? 1 : 0);
+    return PTAP_OK;
+  }
   return fail(PTAP_ERR_VALUE, std::string("unknown plan option '") + key + "'");
 }
 
@@ -2008,6 +2013,57 @@ ptap_status ptap_spgemm_ap_numeric(const ptap_operands *ops, const int64_t *row_
     int s = 0;
     if ((rc = read_status(&tmp, st, &s)) != PTAP_OK) break;
     if (s) rc = status_to_error(s, "spgemm numeric");
+  } while (0);
+  cudaStreamSynchronize(st);
+  for (auto &kv : tmp.allocs) cudaFree(kv.first);
+  tmp.allocs.clear();
+  cudaFree(tmp.d_status);
+  cudaFree(tmp.d_u64);
+  tmp.d_status = nullptr;
+  tmp.d_u64 = nullptr;
+  return rc;
+}
+
+// ---- standalone transpose (reference transpose_with_permutation) ------------
+ptap_status ptap_transpose(int64_t nrows, int64_t ncols, const int64_t *rp, const int32_t *col, const double *val,
+                           int64_t nnz, int64_t *t_rp, int32_t *t_col, int64_t *perm, double *t_val, void *stream) {
+  if (nrows < 0 || ncols < 0 || nnz < 0 || !rp || !t_rp || (nnz > 0 && (!col || !t_col || !perm)))
+    return fail(PTAP_ERR_VALUE, "transpose: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  ptap_plan tmp;
+  tmp.nloc = nrows;
+  if (cudaMalloc(&tmp.d_status, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tmp.d_u64, 24 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(PTAP_ERR_CUDA, "alloc");
+  cudaMemset(tmp.d_status, 0, sizeof(int));
+  ptap_status rc = PTAP_OK;
+  int64_t *cnt = nullptr, *scratch = nullptr;
+  int32_t *wide = nullptr;
+  do {
+    if ((rc = palloc(&tmp, &cnt, ncols, CAT_TRANSIENT, st)) != PTAP_OK) break;
+    if ((rc = palloc(&tmp, &scratch, scan_scratch_elems(ncols), CAT_TRANSIENT, st)) != PTAP_OK) break;
+    cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ncols > 0 ? ncols : 1), st);
+    if (nnz > 0) launch_count_cols(nnz, col, cnt, st);
+    scan_exclusive(cnt, t_rp, ncols, scratch, st);
+    cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ncols > 0 ? ncols : 1), st);
+    if (nnz > 0) {
+      launch_transpose_scatter(nrows, rp, col, t_rp, cnt, t_col, perm, st);
+      // rows of the transpose in ascending source row (a stable transpose:
+      // perm is the stable argsort of the columns, as in the reference)
+      if ((rc = palloc(&tmp, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st)) != PTAP_OK) break;
+      cudaMemsetAsync(tmp.d_u64 + 6, 0, sizeof(unsigned long long), st);
+      launch_sort_rows(ncols, t_rp, t_col, perm, wide, tmp.d_u64 + 6, st);
+      unsigned long long nwide = 0;
+      cudaMemcpyAsync(&nwide, tmp.d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      launch_sort_rows_block((int64_t)nwide, wide, t_rp, t_col, perm, tmp.d_status, st);
+      if (val && t_val) launch_gather(nnz, perm, val, t_val, st);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { rc = fail(PTAP_ERR_CUDA, std::string("transpose: ") + cudaGetErrorString(e)); break; }
+    int s = 0;
+    if ((rc = read_status(&tmp, st, &s)) != PTAP_OK) break;
+    if (s) rc = status_to_error(s, "transpose");
   } while (0);
   cudaStreamSynchronize(st);
   for (auto &kv : tmp.allocs) cudaFree(kv.first);

@@ -84,6 +84,29 @@ class DeviceCsr:
     def struct(self) -> _lib.Csr:
         return _lib.Csr(self.nrows, self.ncols, self.nnz, _ptr(self.row_ptr), _ptr(self.col), _ptr(self.val))
 
+    def transpose_with_permutation(self):
+        """Device transpose plus the permutation mapping this block's values
+        to the transpose's (reference CsrMatrix.transpose_with_permutation,
+        src/sparse.py:165-178: ``t.val[:] = self.val[perm]`` refreshes it).
+        Runs ``ptap_transpose`` (count, scan, scatter, per-row sort)."""
+        import ctypes
+
+        torch = _torch()
+        dev = self.row_ptr.device
+        n = self.nnz
+        t_rp = torch.zeros(self.ncols + 1, dtype=torch.int64, device=dev)
+        t_col = torch.empty(n, dtype=torch.int32, device=dev)
+        perm = torch.empty(n, dtype=torch.int64, device=dev)
+        t_val = None if self.val is None else torch.empty(n, dtype=torch.float64, device=dev)
+        L = _lib.load()
+        _lib.check(L.ptap_transpose(self.nrows, self.ncols, _ptr(self.row_ptr), _ptr(self.col), _ptr(self.val), n,
+                                    _ptr(t_rp), _ptr(t_col), _ptr(perm), _ptr(t_val),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "transpose")
+        return DeviceCsr(self.ncols, self.nrows, t_rp, t_col, t_val), perm
+
+    def transpose(self) -> "DeviceCsr":
+        return self.transpose_with_permutation()[0]
+
 
 class DeviceLocalMatrix:
     """Device image of a reference ``LocalMatrix``."""

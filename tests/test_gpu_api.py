@@ -245,3 +245,29 @@ def test_streamed_path_falls_back_when_rows_not_range_addressable():
     ip = plan.c_alloc.local.diag.row_offsets
     assert row_scaled_err(ip, c2, c1) <= RUN_TOL
     assert plan.counters.numeric_runs == 2
+
+
+def test_device_transpose_matches_reference_semantics():
+    """DeviceCsr.transpose_with_permutation (ptap_transpose) against the
+    host definition of the reference (stable argsort of the columns,
+    src/sparse.py:165-178): identical structure, permutation and values."""
+    from paper_1905_08423_b200.device import DeviceCsr
+    rng = np.random.default_rng(3)
+    for (n, m, dens) in ((40, 25, 0.2), (1000, 3000, 0.003), (5, 7, 0.0)):
+        mask = rng.random((n, m)) < dens
+        rows, cols = np.nonzero(mask)
+        ip = np.zeros(n + 1, np.int64)
+        np.add.at(ip, rows + 1, 1)
+        ip = np.cumsum(ip)
+        vals = rng.standard_normal(rows.size)
+        A = pk.CsrMatrix(n, m, ip, cols, vals)
+        d = DeviceCsr.from_host(A, "cuda")
+        t, perm = d.transpose_with_permutation()
+        want_perm = np.argsort(cols, kind="stable")
+        want_ip = np.zeros(m + 1, np.int64)
+        np.add.at(want_ip, cols + 1, 1)
+        want_ip = np.cumsum(want_ip)
+        assert np.array_equal(t.row_ptr.cpu().numpy(), want_ip)
+        assert np.array_equal(t.col.cpu().numpy(), rows[want_perm])
+        assert np.array_equal(perm.cpu().numpy(), want_perm)
+        assert np.array_equal(t.val.cpu().numpy().view(np.uint64), vals[want_perm].view(np.uint64))
