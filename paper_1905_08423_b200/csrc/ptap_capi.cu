@@ -130,6 +130,8 @@ struct ptap_plan {
   TileArgs ta{};
   int64_t max_nap = 0;              // widest AP row
   int64_t qmap_bytes = 0;           // tile gather maps (interned)
+  bool smap_deferred = false;       // slot-map buffer not allocated yet (chunked or allocated on first use)
+  bool pmap_interned = false;       // position maps built and interned chunk by chunk
   std::vector<std::pair<int64_t, int64_t>> qa_runs;  // several ranks: runs of rows without A_o/P_o (q4a)
   int32_t *qa_rest = nullptr;       // ... and the other bin-0 rows (q4)
   int64_t qa_rest_n = 0;
@@ -784,7 +786,10 @@ ptap_status prepare_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, 
   pfree(p, unused, st);
   pfree(p, scratch, st);
   p->smap_bytes = tot[0];
-  CKS(palloc(p, &p->maps.smap, tot[0] + 16, CAT_PLAN, st));  // padded: staged word-wise
+  // a rank that sends nothing writes its slot maps in symbolic_local, which
+  // builds them chunk by chunk when it can: the full buffer is deferred
+  p->smap_deferred = ops->p_off.nnz == 0 && !getenv("PTAP_NO_MAP_CHUNKS");
+  if (!p->smap_deferred) CKS(palloc(p, &p->maps.smap, tot[0] + 16, CAT_PLAN, st));  // padded: staged word-wise
   CKS(palloc(p, &p->maps.nap, p->nloc, CAT_PLAN, st));
   CKS(palloc(p, &p->pat, tot[1], CAT_TRANSIENT, st));
   tr.mark(st, "  maps: alloc 2");
@@ -1113,7 +1118,9 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     if (!p->smap_interned)
       CKS(intern_map(p, p->maps.smap, p->maps.smap_rp, p->nloc, p->smap_bytes, true, &p->smap_bytes, st));
     p->smap_interned = true;
-    CKS(intern_map(p, p->maps.pmap, p->maps.pmap_rp, p->nloc, p->pmap_bytes, false, &p->pmap_bytes, st));
+    if (!p->pmap_interned)
+      CKS(intern_map(p, p->maps.pmap, p->maps.pmap_rp, p->nloc, p->pmap_bytes, false, &p->pmap_bytes, st));
+    p->pmap_interned = true;
     p->cnt.numeric_path = 1;
     p->cnt.map_bytes = p->smap_bytes + p->pmap_bytes;
     CKS(build_tile(p, op, ops, st));
@@ -1190,13 +1197,174 @@ ptap_status c_rows_by_union(ptap_plan *p, const int64_t *t_rp, const int32_t *t_
 // receives): maps-only outer pass over the local rows, P_d^T, then the row
 // unions of the contributors' sorted AP rows, which also write the position
 // maps.
+// the deferred slot-map buffer, full size, for the unchunked passes
+ptap_status ensure_smap(ptap_plan *p, cudaStream_t st) {
+  if (!p->smap_deferred) return PTAP_OK;
+  CKS(palloc(p, &p->maps.smap, p->smap_bytes + 16, CAT_PLAN, st));
+  p->mo.smap = p->maps.smap;
+  p->smap_deferred = false;
+  return PTAP_OK;
+}
+
+// The maps-only outer-product pass over row chunks, each chunk's slot maps
+// interned as soon as they are written, so the per-row maps (1.5 GB on
+// config 3) never exist at once: every row of the plan is in the identity
+// bin 0 (one-rank structure).  The chunk pools are concatenated (a row class
+// recurs in every chunk, at ~10 KB per chunk on config 3).
+ptap_status chunked_slot_maps(ptap_plan *p, const Ops &op, cudaStream_t st, bool *done) {
+  *done = false;
+  BinSet &bs = p->bins_local;
+  const int64_t n = p->nloc;
+  if (!p->smap_deferred || !p->q4_sym || !bs.identity0 || bs.count[0] != n || bs.count[1] || bs.count[2] ||
+      bs.count[3] || n < 4 * 65536 || getenv("PTAP_NO_INTERN"))
+    return PTAP_OK;
+  p->smap_deferred = false;
+  const int K = std::max<int64_t>(2, std::min<int64_t>(16, p->smap_bytes >> 27));  // ~128 MB chunks
+  std::vector<int64_t> rb(K + 1), off(K + 1);
+  for (int c = 0; c <= K; ++c) rb[c] = n * c / K;
+  for (int c = 0; c <= K; ++c)
+    CK(cudaMemcpyAsync(&off[c], p->maps.smap_rp + rb[c], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t *gout = nullptr;
+  CKS(palloc(p, &gout, n + 1, CAT_PLAN, st));
+  std::vector<uint8_t *> pools(K, nullptr);
+  std::vector<int64_t> pbytes(K, 0);
+  int64_t cum = 0;
+  Arena none{nullptr, 0};
+  for (int c = 0; c < K; ++c) {
+    const int64_t r0 = rb[c], r1 = rb[c + 1], nc = r1 - r0;
+    const int64_t base = off[c] & ~int64_t(3), total = off[c + 1] - base;
+    uint8_t *chunk = nullptr;
+    int64_t *crp = nullptr;
+    CKS(palloc(p, &chunk, total + 16, CAT_TRANSIENT, st));
+    MapOut mc = p->mo;
+    mc.smap = chunk - base;  // the kernel writes at smap_rp[i]
+    CK(launch_outer_symbolic_q4(op, nullptr, (unsigned long long)nc, 0, 1, none, none, mc, p->d_status, st,
+                                (int)r0));
+    CKS(palloc(p, &crp, nc + 1, CAT_TRANSIENT, st));
+    CK(launch_offsets_shift(nc + 1, p->maps.smap_rp + r0, base, -1, crp, st));
+    int64_t pb = 0;
+    CKS(intern_map(p, chunk, crp, nc, total, true, &pb, st));
+    pb = (pb + 3) & ~int64_t(3);
+    CK(launch_offsets_shift(nc, crp, 0, cum, gout + r0, st));
+    pfree(p, crp, st);
+    pools[c] = chunk;
+    pbytes[c] = pb;
+    cum += pb;
+    p->cnt.kernel_launches += 3;
+  }
+  uint8_t *pool = nullptr;
+  CKS(palloc(p, &pool, cum + 16, CAT_PLAN, st));
+  int64_t at = 0;
+  for (int c = 0; c < K; ++c) {
+    if (pbytes[c]) CK(cudaMemcpyAsync(pool + at, pools[c], pbytes[c], cudaMemcpyDeviceToDevice, st));
+    at += pbytes[c];
+    pfree(p, pools[c], st);
+  }
+  CK(cudaMemsetAsync(pool + cum, 0, 16, st));
+  pfree(p, p->maps.smap_rp, st);
+  p->maps.smap = pool;
+  p->maps.smap_rp = gout;
+  p->smap_bytes = cum;
+  p->mo.smap = nullptr;
+  p->mo.smap_rp = nullptr;
+  p->smap_interned = true;
+  *done = true;
+  return PTAP_OK;
+}
+
+// Position maps chunk by chunk once C's pattern is known: each fine-row
+// window's maps are found by binary search in its target C rows
+// (k_build_pmap) and interned at once, so the per-row maps (0.87 GB on
+// config 3) never exist together with the AP patterns they are built from.
+ptap_status chunked_pos_maps(ptap_plan *p, const Ops &op, cudaStream_t st, bool *done) {
+  *done = false;
+  const int64_t n = p->nloc;
+  if (getenv("PTAP_NO_MAP_CHUNKS") || getenv("PTAP_NO_INTERN") || op.po_rp != nullptr || n < 4 * 65536) return PTAP_OK;
+  unsigned long long *mx = p->d_u64 + 12;
+  CK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
+  CK(launch_max_rowlen(p->ncl, p->c_rp, mx, st));
+  unsigned long long cmax = 0;
+  CK(cudaMemcpyAsync(&cmax, mx, sizeof(cmax), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (cmax > 256) return PTAP_OK;  // positions must fit a byte: the caller takes the hash path
+  int64_t *plen = nullptr, *scratch = nullptr, *unused = nullptr, *prp = nullptr;
+  CKS(palloc(p, &plen, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &unused, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &scratch, scan_scratch_elems(n), CAT_TRANSIENT, st));
+  CK(launch_map_lengths(n, op.pd_rp, op.po_rp, p->apub, p->ap_nnz, unused, plen, st));
+  CKS(palloc(p, &prp, n + 1, CAT_TRANSIENT, st));
+  CK(scan_exclusive(plen, prp, n, scratch, st));
+  pfree(p, plen, st);
+  pfree(p, unused, st);
+  pfree(p, scratch, st);
+  int64_t tot = 0;
+  CK(cudaMemcpyAsync(&tot, prp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int K = (int)std::max<int64_t>(2, std::min<int64_t>(16, tot >> 27));
+  std::vector<int64_t> rb(K + 1), off(K + 1);
+  for (int c = 0; c <= K; ++c) rb[c] = n * c / K;
+  for (int c = 0; c <= K; ++c) CK(cudaMemcpyAsync(&off[c], prp + rb[c], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t *gout = nullptr;
+  CKS(palloc(p, &gout, n + 1, CAT_PLAN, st));
+  std::vector<uint8_t *> pools(K, nullptr);
+  std::vector<int64_t> pbytes(K, 0);
+  int64_t cum = 0;
+  OuterTargets tg{p->c_rp, p->c_col, nullptr, 0, nullptr, nullptr, nullptr, nullptr};
+  for (int c = 0; c < K; ++c) {
+    const int64_t r0 = rb[c], r1 = rb[c + 1], nc = r1 - r0;
+    const int64_t base = off[c] & ~int64_t(3), total = off[c + 1] - base;
+    uint8_t *chunk = nullptr;
+    int64_t *crp = nullptr;
+    CKS(palloc(p, &chunk, total + 16, CAT_TRANSIENT, st));
+    MapArgs mc = p->maps;
+    mc.pmap = chunk - base;
+    mc.pmap_rp = prp;
+    CK(launch_build_pmap(op, (unsigned long long)nc, mc, p->mo, tg, p->d_status, st, r0));
+    CKS(palloc(p, &crp, nc + 1, CAT_TRANSIENT, st));
+    CK(launch_offsets_shift(nc + 1, prp + r0, base, -1, crp, st));
+    int64_t pb = 0;
+    CKS(intern_map(p, chunk, crp, nc, total, false, &pb, st));
+    pb = (pb + 3) & ~int64_t(3);
+    CK(launch_offsets_shift(nc, crp, 0, cum, gout + r0, st));
+    pfree(p, crp, st);
+    pools[c] = chunk;
+    pbytes[c] = pb;
+    cum += pb;
+    p->cnt.kernel_launches += 3;
+  }
+  pfree(p, prp, st);
+  uint8_t *pool = nullptr;
+  CKS(palloc(p, &pool, cum + 16, CAT_PLAN, st));
+  int64_t at = 0;
+  for (int c = 0; c < K; ++c) {
+    if (pbytes[c]) CK(cudaMemcpyAsync(pool + at, pools[c], pbytes[c], cudaMemcpyDeviceToDevice, st));
+    at += pbytes[c];
+    pfree(p, pools[c], st);
+  }
+  CK(cudaMemsetAsync(pool + cum, 0, 16, st));
+  p->maps.pmap = pool;
+  p->maps.pmap_rp = gout;
+  p->pmap_bytes = cum;
+  CKS(palloc(p, &p->maps.po_srow, 1, CAT_PLAN, st));  // no P_o entries
+  p->pmap_ready = true;
+  p->pmap_interned = true;
+  *done = true;
+  return PTAP_OK;
+}
+
 ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st, Tracer *tr) {
   Arena none{nullptr, 0};
-  CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
-    if (s.bin == 0 && p->q4_sym && p->mo.smap)
-      return launch_outer_symbolic_q4(op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
-    return launch_outer_symbolic(s, op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
-  }));
+  bool chunked = false;
+  CKS(chunked_slot_maps(p, op, st, &chunked));
+  if (!chunked) CKS(ensure_smap(p, st));
+  if (!chunked)
+    CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+      if (s.bin == 0 && p->q4_sym && p->mo.smap)
+        return launch_outer_symbolic_q4(op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
+      return launch_outer_symbolic(s, op, rows, n, 0, 1, none, none, p->mo, p->d_status, st);
+    }));
   p->cnt.symbolic_row_kernel_calls += p->bins_local.selected;
   int s0 = 0;
   CKS(read_status(p, st, &s0));
@@ -1226,10 +1394,19 @@ ptap_status c_by_unions(ptap_plan *p, const Ops &op, const ptap_operands *ops, c
   pfree(p, cnt, st);
   pfree(p, scratch, st);
   tr->mark(st, "P_d^T");
-  ptap_status ret = c_rows_by_union(p, t_rp, t_row, p->mo.pat_rp, p->mo.pat, &op, ops, st);
+  // position maps: chunked after the unions (bounded memory), or written by
+  // the unions' fill pass
+  const bool chunk_pm = !getenv("PTAP_NO_MAP_CHUNKS") && !getenv("PTAP_NO_INTERN") && op.po_rp == nullptr &&
+                        p->nloc >= 4 * 65536;
+  ptap_status ret = c_rows_by_union(p, t_rp, t_row, p->mo.pat_rp, p->mo.pat, chunk_pm ? nullptr : &op, ops, st);
   pfree(p, t_rp, st);
   pfree(p, t_row, st);
   tr->mark(st, "C rows by unions");
+  if (ret == PTAP_OK && chunk_pm) {
+    bool done = false;
+    CKS(chunked_pos_maps(p, op, st, &done));
+    tr->mark(st, "position maps (chunked)");
+  }
   return ret;
 }
 
@@ -1571,6 +1748,7 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   {
   Arena &la = p->local_arena;
   if (local_loop_here) {
+    CKS(ensure_smap(p, st));
     CKS(with_arena_retry(p, la, st, [&]() -> ptap_status {
       return for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
         Arena none{nullptr, 0};
@@ -1608,8 +1786,6 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   la = Arena{nullptr, 0};
   }
 c_allocated:
-  CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
-  CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
   if (recv && recv->nrows > 0) {
     CKS(palloc(p, &p->r_slot, rnnz, CAT_PLAN, st));
     CK(launch_merge_slots(recv->nrows, recv->rows, recv->row_ptr, recv->col, p->c_lo, p->c_rp, p->c_col, p->r_slot,
@@ -1630,6 +1806,9 @@ c_allocated:
   if (p->alg != PTAP_TWO_STEP) CKS(build_maps(p, op, ops, st));
   tr.mark(st, "position maps");
   CKS(build_q4a_runs(p, op, ops, st));
+  // C's values last: the position maps' transient peak is over by now
+  CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
+  CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
   if (p->rows_unstructured && !(p->alg != PTAP_TWO_STEP && p->mapped) && !getenv("PTAP_NO_ROW_ORDER")) {
     // an operator whose rows do not repeat: visit rows in aggregate order
     // (k_row_order_keys) -- the hash numeric path, and two-step's C~ = A P

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic(Ops op, const int32_t *r
 // row), the position of each AP slot of row i inside row J, found by a
 // binary search of the row's sorted pattern.  8-lane groups, 4 rows per warp.
 __global__ void __launch_bounds__(256) k_build_pmap(Ops op, unsigned long long nrows, MapArgs mp, MapOut mo,
-                                                    OuterTargets tg, int *status) {
+                                                    OuterTargets tg, int *status, int64_t row0) {
   constexpr int G = 8;
   // the row's sorted AP pattern (<= 255 columns) is searched from shared memory
   __shared__ int32_t spat_all[256 / G][256];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) k_build_pmap(Ops op, unsigned long long n
        r0 += (unsigned long long)gridDim.x * gpc) {
     unsigned long long ridx = r0 + lane_id() / G;
     if (ridx >= nrows) continue;
-    int64_t i = (int64_t)ridx;
+    int64_t i = row0 + (int64_t)ridx;
     int64_t pd0 = op.pd_rp[i], pd1 = op.pd_rp[i + 1], po0 = 0, po1 = 0;
     if (op.po_rp) { po0 = op.po_rp[i]; po1 = op.po_rp[i + 1]; }
     int ndP = (int)(pd1 - pd0), nP = ndP + (int)(po1 - po0);
@@ -1026,7 +1026,7 @@ __device__ __forceinline__ void sq_walk(const Ops &op, SqWarp &W, int i, int gl,
 
 __global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t *rows, unsigned long long nrows,
                                                            int do_send, int do_local, Arena local, Arena send,
-                                                           MapOut mo, int *status) {
+                                                           MapOut mo, int *status, int row0) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int G = SQ_G;
   const int lane = lane_id(), gl = lane & (G - 1), r = lane / G;
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t
   const int total = (int)nrows;
   for (int r0 = (blockIdx.x * nwarps + warp) * SQ_R; r0 < total; r0 += gridDim.x * nwarps * SQ_R) {
     const int ridx = r0 + r;
-    int i = ridx < total ? (rows ? rows[ridx] : ridx) : -1;
+    int i = ridx < total ? (rows ? rows[ridx] : row0 + ridx) : -1;
     int pd0 = 0, pd1 = 0, po0 = 0, po1 = 0;
     if (i >= 0) {
       pd0 = (int)__ldg(op.pd_rp + i); pd1 = (int)__ldg(op.pd_rp + i + 1);
@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(256) k_outer_symbolic_q4(Ops op, const int32_t
 
 cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigned long long nrows, int do_send,
                                      int do_local, Arena local, Arena send, const MapOut &mo, int *status,
-                                     cudaStream_t stream) {
+                                     cudaStream_t stream, int row0) {
   if (nrows == 0) return cudaSuccess;
   const int warps = 8;
   const size_t sm = (size_t)warps * sizeof(SqWarp);
@@ -1155,7 +1155,7 @@ cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigne
   unsigned long long grid = (nrows + rpc - 1) / rpc;
   grid = std::min<unsigned long long>(grid, 148ull * 64);
   k_outer_symbolic_q4<<<(int)grid, warps * 32, sm, stream>>>(op, rows, nrows, do_send, do_local, local, send, mo,
-                                                             status);
+                                                             status, row0);
   return cudaGetLastError();
 }
 
@@ -1650,11 +1650,11 @@ cudaError_t launch_ptc_est(int64_t nrows, const int32_t *target_map, int64_t tar
 }
 
 cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const MapArgs &mp, const MapOut &mo,
-                              const OuterTargets &tg, int *status, cudaStream_t st) {
+                              const OuterTargets &tg, int *status, cudaStream_t st, int64_t row0) {
   if (nrows == 0) return cudaSuccess;
   unsigned long long grid = (nrows + 31) / 32;
   if (grid > 148ull * 64) grid = 148ull * 64;
-  k_build_pmap<<<(int)grid, 256, 0, st>>>(op, nrows, mp, mo, tg, status);
+  k_build_pmap<<<(int)grid, 256, 0, st>>>(op, nrows, mp, mo, tg, status, row0);
   return cudaGetLastError();
 }
 

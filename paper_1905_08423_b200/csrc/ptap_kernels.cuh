@@ -83,7 +83,9 @@ cudaError_t launch_retry_est(int64_t n, const int64_t *ap_nnz, const int64_t *ap
                              unsigned long long *nretry, cudaStream_t st);
 cudaError_t launch_outer_symbolic_q4(const Ops &op, const int32_t *rows, unsigned long long nrows, int do_send,
                                      int do_local, Arena local, Arena send, const MapOut &mo, int *status,
-                                     cudaStream_t stream);
+                                     cudaStream_t stream, int row0 = 0);
+cudaError_t launch_offsets_shift(int64_t n, const int64_t *in, int64_t sub, int64_t add_packed, int64_t *out,
+                                 cudaStream_t st);
 cudaError_t launch_c_union(bool fill, int64_t ncl, const int64_t *t_rp, const int32_t *t_row, const int64_t *pat_rp,
                            const int32_t *pat, const uint8_t *nap, int64_t *cnt, const int64_t *c_rp, int32_t *c_col,
                            const int64_t *pd_rp, const int32_t *pd_col, const int64_t *pmap_rp, uint8_t *pmap,
@@ -94,7 +96,7 @@ cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int
                                   int do_send, int do_local, Arena local, Arena send, const MapOut &mo, int *status,
                                   cudaStream_t stream);
 cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const MapArgs &mp, const MapOut &mo,
-                              const OuterTargets &tg, int *status, cudaStream_t st);
+                              const OuterTargets &tg, int *status, cudaStream_t st, int64_t row0 = 0);
 cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                  int do_send, int do_local, const OuterTargets &tg, int *status,
                                  cudaStream_t stream);

@@ -1178,6 +1178,24 @@ __global__ void k_pack_offsets(int64_t n, const int64_t *rp, int64_t *out) {
   if (i < n) out[i] = rp[i] | ((rp[i + 1] - rp[i]) << 40);
 }
 
+// out[i] = in[i] - sub (plain offsets) or, with add_packed >= 0, packed
+// entries (offset | len << 40) with add_packed added to the offset part
+__global__ void k_offsets_shift(int64_t n, const int64_t *in, int64_t sub, int64_t add_packed, int64_t *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (add_packed < 0) {
+    out[i] = in[i] - sub;
+  } else {
+    const unsigned long long x = (unsigned long long)in[i];
+    out[i] = (int64_t)(((x & SMAP_OFF_MASK) + (unsigned long long)add_packed) | (x & ~SMAP_OFF_MASK));
+  }
+}
+cudaError_t launch_offsets_shift(int64_t n, const int64_t *in, int64_t sub, int64_t add_packed, int64_t *out,
+                                 cudaStream_t st) {
+  if (n > 0) k_offsets_shift<<<nb(n, 256), 256, 0, st>>>(n, in, sub, add_packed, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_offsets(int64_t n, const int64_t *rp, int64_t *out, cudaStream_t st) {
   if (n > 0) k_pack_offsets<<<nb(n, 256), 256, 0, st>>>(n, rp, out);
   return cudaGetLastError();
