@@ -539,8 +539,8 @@ def our_arm(args):
                          "deterministic": vplan.deterministic, "memory": vmem}
             if name in ("allatonce_deterministic", "allatonce_hash"):
                 out[name]["gflops"] = flops / (vms * 1e-3) / 1e9
-                if ctx.nranks == 1:
-                    det_val = vval.cpu().numpy()
+            if name == "allatonce_deterministic" and ctx.nranks == 1:
+                det_val = vval.cpu().numpy()
             del vplan, vrp, vval
             gc.collect()
             torch.cuda.synchronize()
