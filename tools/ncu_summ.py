@@ -1,7 +1,7 @@
 """Summarise an ncu report of a numeric kernel: per-row instruction and L1
 wavefront budget, plus the top stall/wavefront SASS lines.
 usage: python tools/ncu_summ.py report.ncu-rep [rows]"""
-import csv, io, subprocess, sys
+import csv, io, os, subprocess, sys
 
 rep = sys.argv[1]
 nrows = float(sys.argv[2]) if len(sys.argv) > 2 else 256.0 ** 3
@@ -56,14 +56,20 @@ def write_summary(rep_path, kernel_desc, out_json, out_txt, nrows_):
     raw_ = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"],
                                                       capture_output=True, text=True).stdout)))
     R_ = dict(zip(raw_[0], raw_[2]))
+    U_ = dict(zip(raw_[0], raw_[1]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
     def g(k):
         try:
             return float(R_[k].replace(",", ""))
         except (KeyError, ValueError):
             return None
-    rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
-    unit_scale = 1e9  # ncu reports dram bytes in GB in this layout
+
+    def gb(k):  # bytes, whatever unit ncu chose for the column
+        v = g(k)
+        return None if v is None else v * scale.get(U_.get(k, "byte"), 1.0)
+    rd, wr = gb("dram__bytes_read.sum"), gb("dram__bytes_write.sum")
+    unit_scale = 1.0
     d = {"kernel": kernel_desc,
          "capture": f"ncu --set full --clock-control none, 1 launch ({os.path.basename(out_txt)})",
          "gpu_time_ms": g("gpu__time_duration.sum"),
