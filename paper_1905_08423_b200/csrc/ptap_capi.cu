@@ -128,6 +128,10 @@ struct ptap_plan {
   const void *img_ptr[11] = {nullptr};
   unsigned long long img_digest = 0;
   TileArgs ta{};
+  LockArgs la{};
+  bool lock = false;                // class-lockstep numeric kernel (ptap_lock.cu) replaces q4a
+  int lock_opt = -1;                // plan option "lockstep": -1 when eligible, 0 never, 1 same as -1
+  int lock_classes = 0;
   int64_t max_nap = 0;              // widest AP row
   int64_t qmap_bytes = 0;           // tile gather maps (interned)
   bool smap_deferred = false;       // slot-map buffer not allocated yet (chunked or allocated on first use)
@@ -1095,6 +1099,122 @@ ptap_status build_tile(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   return PTAP_OK;
 }
 
+// ---- class-lockstep numeric plan (ptap_lock.cu) ------------------------------
+void free_lock(ptap_plan *p, cudaStream_t st) {
+  LockArgs &l = p->la;
+  pfree(p, l.pq, st); pfree(p, l.Q, st); pfree(p, l.cbQ, st); pfree(p, l.rowinfo, st);
+  pfree(p, l.cls, st); pfree(p, l.fold, st); pfree(p, l.outer, st); pfree(p, l.ltab, st);
+  l = LockArgs{};
+  p->lock = false;
+}
+
+// Eligible: the q4a plan (one-rank structure, A rows <= 32 entries) with
+// interned maps, AP rows <= 32 slots, P rows <= 8 entries, fewer than 32768
+// row classes, the C-row-start map, and a tile that fits shared memory.
+ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+  p->lock = false;
+  if (getenv("PTAP_NO_LOCK") || p->lock_opt == 0) return PTAP_OK;
+  if (!p->mapped || !p->q4a || p->tile || p->alg == PTAP_TWO_STEP || p->max_nap > 32 || !p->maps.cbase)
+    return PTAP_OK;
+  const int64_t n = p->nloc, pnnz = ops->p_diag.nnz;
+  if (n <= 0 || p->ncl <= 0 || pnnz <= 0 || pnnz >= INT32_MAX || ops->a_diag.nnz >= INT32_MAX ||
+      n >= INT32_MAX - 2 * LOCK_TILE || p->c_nnz >= INT32_MAX - 256)
+    return PTAP_OK;
+  LockArgs &l = p->la;
+  l = LockArgs{};
+  const int ntiles = (int)((n + LOCK_TILE - 1) / LOCK_TILE);
+  const int nb = (int)((n + 255) / 256);
+  unsigned long long *st8 = nullptr;  // [0] classes, [1] fold entries, [2] outer words, [3] claims, [4] bad, [5] largest tile
+  uint8_t *plen8 = nullptr;
+  int32_t *blkcnt = nullptr, *ltab = nullptr, *slot2cls = nullptr;
+  uint32_t *pq = nullptr, *rep = nullptr, *reps = nullptr, *rowinfo = nullptr;
+  unsigned long long *keys = nullptr;
+  uint16_t *slot_of = nullptr;
+  auto drop_transient = [&]() {
+    pfree(p, st8, st); pfree(p, plen8, st); pfree(p, blkcnt, st); pfree(p, slot2cls, st);
+    pfree(p, rep, st); pfree(p, reps, st); pfree(p, keys, st); pfree(p, slot_of, st);
+  };
+  CKS(palloc(p, &st8, 8, CAT_TRANSIENT, st));
+  CK(cudaMemsetAsync(st8, 0, 8 * sizeof(unsigned long long), st));
+  CKS(palloc(p, &plen8, n, CAT_TRANSIENT, st));
+  CKS(palloc(p, &blkcnt, (int64_t)LOCK_NLEN * nb, CAT_TRANSIENT, st));
+  CKS(palloc(p, &ltab, 2 * LOCK_NLEN, CAT_PLAN, st));
+  CKS(palloc(p, &pq, n, CAT_PLAN, st));
+  l.ltab = ltab; l.pq = pq;
+  CK(launch_lock_qlayout(n, op.pd_rp, plen8, blkcnt, ltab, pq, st8 + 4, st));
+  pfree(p, blkcnt, st);
+  CKS(palloc(p, &keys, LOCK_TABLE, CAT_TRANSIENT, st));
+  CKS(palloc(p, &rep, LOCK_TABLE, CAT_TRANSIENT, st));
+  CKS(palloc(p, &reps, LOCK_TABLE, CAT_TRANSIENT, st));
+  CKS(palloc(p, &slot2cls, LOCK_TABLE, CAT_TRANSIENT, st));
+  CKS(palloc(p, &slot_of, n, CAT_TRANSIENT, st));
+  CK(launch_lock_classes(op, plen8, p->maps.smap_rp, p->maps.pmap_rp, keys, rep, LOCK_TABLE, slot_of, slot2cls, reps,
+                         st8, st8 + 4, st));
+  unsigned long long h[8];
+  CK(cudaMemcpyAsync(h, st8, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->cnt.kernel_launches += 7;
+  if (h[4] != 0 || h[3] > LOCK_TABLE / 2 || h[0] == 0) {
+    if (getenv("PTAP_TRACE"))
+      fprintf(stderr, "[ptap] lockstep plan: not eligible (%llu classes, %llu flagged)\n", h[0], h[4]);
+    drop_transient();
+    free_lock(p, st);
+    return PTAP_OK;
+  }
+  const int ncls = (int)h[0];
+  LockClass *cls = nullptr;
+  CKS(palloc(p, &cls, ncls, CAT_PLAN, st));
+  l.cls = cls;
+  CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, st));
+  CKS(palloc(p, &rowinfo, n, CAT_PLAN, st));
+  l.rowinfo = rowinfo;
+  CK(launch_lock_rowinfo(n, op.ad_rp, slot_of, slot2cls, rowinfo, st8 + 5, st));
+  CK(cudaMemcpyAsync(h, st8, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->cnt.kernel_launches += 2;
+  l.nloc = (int32_t)n;
+  l.ntiles = ntiles;
+  l.acap = (int32_t)((h[5] + 4 + 3) & ~3ull);
+  l.aps = (int32_t)(std::max<int64_t>(1, p->max_nap) | 1);
+  if (h[4] != 0 || lock_smem_bytes(l) > 200 * 1024 || h[1] >= (1ull << 31) || h[2] >= (1ull << 31)) {
+    if (getenv("PTAP_TRACE"))
+      fprintf(stderr, "[ptap] lockstep plan: not eligible (%llu flagged, tile of %llu entries)\n", h[4], h[5]);
+    drop_transient();
+    free_lock(p, st);
+    return PTAP_OK;
+  }
+  uint2 *fold = nullptr;
+  uint32_t *outer = nullptr;
+  CKS(palloc(p, &fold, (int64_t)h[1] + 8, CAT_PLAN, st));
+  CKS(palloc(p, &outer, (int64_t)h[2] + 32, CAT_PLAN, st));
+  l.fold = fold; l.outer = outer;
+  CK(launch_lock_programs(ncls, op, plen8, p->maps, reps, ltab, cls, fold, outer, st));
+  drop_transient();
+  // the C row starts in Q order replace the per-entry map of the q4a kernel
+  int32_t *cbq = nullptr;
+  double *Q = nullptr;
+  CKS(palloc(p, &cbq, pnnz, CAT_PLAN, st));
+  CK(launch_lock_permute_i32(n, op.pd_rp, pq, ltab, p->maps.cbase, cbq, st));
+  l.cbQ = cbq;
+  pfree(p, p->maps.cbase, st);
+  CKS(palloc(p, &Q, pnnz, CAT_PLAN, st));
+  l.Q = Q;
+  p->cnt.kernel_launches += 3;
+  p->lock = true;
+  p->lock_classes = ncls;
+  if (getenv("PTAP_TRACE"))
+    fprintf(stderr,
+            "[ptap] lockstep plan: %d tiles, %d classes, programs %llu + %llu entries, tile <= %d A entries, "
+            "smem %zu B\n",
+            ntiles, ncls, h[1], h[2], l.acap, lock_smem_bytes(l));
+  return PTAP_OK;
+}
+
+// the lockstep kernel stages A by TMA bulk copies: 16-byte aligned arrays
+static bool lock_usable(const ptap_plan *p, const Ops &op) {
+  return p->lock && (((uintptr_t)op.ad_col | (uintptr_t)op.ad_val) & 15) == 0;
+}
+
 // Part 2 (C and the staging allocated): position maps (unless the row-union
 // pass already wrote them), then drop the transient patterns.  Falls back to
 // the hash path if a target row is wider than a byte can address.
@@ -1131,6 +1251,8 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     CKS(palloc(p, &p->maps.cbase, ops->p_diag.nnz, CAT_PLAN, st));
     CK(launch_build_cbase(ops->p_diag.nnz, op.pd_col, p->c_rp, p->maps.cbase, st));
     p->cnt.kernel_launches++;
+    CKS(build_lock(p, op, ops, st));
+    if (p->lock) p->cnt.numeric_path = 3;
   }
   if (!ok) {
     pfree(p, p->maps.smap_rp, st);
@@ -1143,6 +1265,7 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
 
 ptap_status free_maps(ptap_plan *p, cudaStream_t st) {
   free_tile(p, st);
+  free_lock(p, st);
   pfree(p, p->maps.smap_rp, st); pfree(p, p->maps.pmap_rp, st);
   pfree(p, p->maps.smap, st); pfree(p, p->maps.pmap, st);
   pfree(p, p->maps.nap, st); pfree(p, p->maps.po_srow, st);
@@ -1517,6 +1640,12 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
           p->cnt.kernel_launches += 2;
           continue;
         }
+        if (lock_usable(p, op)) {  // rows of one class in lockstep; P's values class-major first
+          CK(launch_lock_permute_f64(p->nloc, op.pd_rp, p->la.pq, p->la.ltab, op.pd_val, p->la.Q, st));
+          CK(launch_lock_numeric(op, p->la, p->c_val, 0, p->la.ntiles, st));
+          p->cnt.kernel_launches += 2;
+          continue;
+        }
         CK(launch_outer_numeric_q4a(op, (unsigned long long)bs.count[q], p->maps, tg, p->d_status, st, 0));
         p->cnt.kernel_launches++;
         continue;
@@ -1571,6 +1700,10 @@ ptap_status ptap_plan_set_option(ptap_plan *p, const char *key, int64_t value) {
   if (!p || !key) return fail(PTAP_ERR_VALUE, "null argument");
   if (!strcmp(key, "deterministic")) {
     p->deterministic = value != 0;
+    return PTAP_OK;
+  }
+  if (!strcmp(key, "lockstep")) {
+    p->lock_opt = value < 0 ? -1 : (value ? 1 : 0);
     return PTAP_OK;
   }
   if (!strcmp(key, "maps")) {
@@ -1921,7 +2054,16 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
   }
   if ((flags & 1) && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
-  if (row_hi > row_lo) {
+  if (lock_usable(p, op) && row_lo % LOCK_TILE == 0 && (row_hi % LOCK_TILE == 0 || row_hi == p->nloc)) {
+    if (flags & 1) {
+      CK(launch_lock_permute_f64(p->nloc, op.pd_rp, p->la.pq, p->la.ltab, op.pd_val, p->la.Q, st));
+      p->cnt.kernel_launches++;
+    }
+    CK(launch_lock_numeric(op, p->la, p->c_val, (int)(row_lo / LOCK_TILE),
+                           (int)((row_hi + LOCK_TILE - 1) / LOCK_TILE), st));
+    p->cnt.kernel_launches++;
+    p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
+  } else if (row_hi > row_lo) {
     if (p->q4a)
       CK(launch_outer_numeric_q4a(op, (unsigned long long)(row_hi - row_lo), p->maps, tg, p->d_status, st,
                                   (int)row_lo));

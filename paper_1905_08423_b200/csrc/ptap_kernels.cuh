@@ -242,4 +242,52 @@ cudaError_t launch_tile_c_last(int64_t ncl, const TileArgs &ta, int32_t *last, c
 cudaError_t launch_tile_scan32(const int32_t *in, int32_t *out, int n, void *scratch, size_t scratch_bytes,
                                cudaStream_t st);
 
+// class-lockstep numeric pass (ptap_lock.cu)
+constexpr int LOCK_TILE = 64;  // fine rows per tile
+constexpr int LOCK_NLEN = 9;   // P row lengths 0..8
+constexpr int LOCK_TABLE = 65536;  // class table slots (a plan with more than half as many classes is not eligible)
+#ifndef PTAP_LOCK_WARPS
+#define PTAP_LOCK_WARPS 2
+#endif
+constexpr int LOCK_W = PTAP_LOCK_WARPS;  // warps per group of 32 rows (<= 7)
+struct __align__(16) LockClass {  // one structural class of fine rows (32 bytes)
+  uint8_t alen, nap, ntg, niter;  // A row length, AP slots, own P entries (targets), outer-program words / 32
+  int32_t tstride;                // rows of P with ntg entries: stride of the row's own entries in Q
+  uint32_t fold_off, outer_off;   // program offsets (entries / words)
+  uint8_t sub[8];                 // fold sub-program w = chunks [sub[w], sub[w+1]) of 8 entries (slot ranges, balanced)
+  uint8_t s0[8];                  // first AP slot of sub-program w
+};
+struct LockArgs {
+  int32_t nloc, ntiles, acap, aps;  // acap: staged A entries per tile, aps: AP buffer stride (doubles, odd)
+  const uint32_t *pq;       // [nloc] Q index of the first entry of P row k
+  double *Q;                // [nnz(P_d)] P's values, class-major (rewritten every pass)
+  const int32_t *cbQ;       // [nnz(P_d)] C row start of every P entry, same order
+  const uint32_t *rowinfo;  // [nloc] per tile, rows sorted by class: class << 8 | row - tile start
+  const LockClass *cls;
+  const uint2 *fold;        // x: A entry*8 | A entry*4 << 8 | valid << 30 | last-of-slot << 31, y: Q offset of the P entry
+  const uint32_t *outer;    // slot*8 | target << 8 | position in the C row << 16
+  const int32_t *ltab;      // [0, NLEN) rows of P per length, [NLEN, 2 NLEN) first Q index per length
+};
+size_t lock_smem_bytes(const LockArgs &la);
+cudaError_t launch_lock_numeric(const Ops &op, const LockArgs &la, double *c_val, int tile_lo, int tile_hi,
+                                cudaStream_t st);
+cudaError_t launch_lock_qlayout(int64_t n, const int64_t *pd_rp, uint8_t *plen8, int32_t *blkcnt, int32_t *ltab,
+                                uint32_t *pq, unsigned long long *bad, cudaStream_t st);
+cudaError_t launch_lock_permute_f64(int64_t n, const int64_t *pd_rp, const uint32_t *pq, const int32_t *ltab,
+                                    const double *src, double *dst, cudaStream_t st);
+cudaError_t launch_lock_permute_i32(int64_t n, const int64_t *pd_rp, const uint32_t *pq, const int32_t *ltab,
+                                    const int32_t *src, int32_t *dst, cudaStream_t st);
+cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64_t *smap_rp, const int64_t *pmap_rp,
+                                unsigned long long *keys, uint32_t *rep, int tbl, uint16_t *slot_of,
+                                int32_t *slot2cls, uint32_t *reps, unsigned long long *out, unsigned long long *bad,
+                                cudaStream_t st);
+cudaError_t launch_lock_headers(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
+                                const uint32_t *reps, const int32_t *ltab, LockClass *cls,
+                                unsigned long long *out, unsigned long long *bad, cudaStream_t st);
+cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
+                                 const uint32_t *reps, const int32_t *ltab, const LockClass *cls, uint2 *fold,
+                                 uint32_t *outer, cudaStream_t st);
+cudaError_t launch_lock_rowinfo(int64_t n, const int64_t *ad_rp, const uint16_t *slot_of, const int32_t *slot2cls,
+                                uint32_t *rowinfo, unsigned long long *amax, cudaStream_t st);
+
 }  // namespace ptapdev
