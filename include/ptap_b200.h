@@ -141,7 +141,7 @@ typedef struct {
     int64_t nnz_staging;
     int64_t mac_ap;                    /* multiply-adds of the A*P rows       */
     int64_t mac_outer;                 /* multiply-adds of the outer products */
-    int64_t numeric_path;              /* all-at-once/merged numeric: 2 deterministic owner-computes, 1 plan maps, 0 hash tables */
+    int64_t numeric_path;              /* all-at-once/merged numeric: 3 plan maps, class-lockstep kernel; 2 deterministic owner-computes; 1 plan maps; 0 hash tables */
     int64_t map_bytes;                 /* plan maps kept (slot + position pools, interned) */
     int64_t row_structures_ppm;        /* distinct row structures per 1e6 sampled rows, -1: not sampled */
 } ptap_counters;
@@ -161,7 +161,12 @@ ptap_status ptap_plan_destroy(ptap_plan *plan);
  *     one-rank structure (counters.numeric_path == 2 when it is in use).
  *   "maps" (-1/0/1): plan maps of the all-at-once / merged numeric pass:
  *     -1 (default) kept when sampled rows repeat, 0 never (hash numeric path,
- *     nothing stored per row), 1 always. */
+ *     nothing stored per row), 1 always.
+ *   "lockstep" (-1/0/1): the class-lockstep numeric kernel (ptap_lock.cu:
+ *     32 rows of one structural class in lockstep, A tiles staged by TMA,
+ *     P's values class-major) for plans with maps and one-rank structure:
+ *     -1/1 (default) when the plan is eligible, 0 never (the per-row mapped
+ *     kernels run instead).  counters.numeric_path == 3 when it is in use. */
 ptap_status ptap_plan_set_option(ptap_plan *plan, const char *key, int64_t value);
 
 /* Symbolic, phase 1: AP-row binning and the send-side structure C_s (all

@@ -13,7 +13,8 @@ import os
 from .errors import DeviceError, OwnershipError, PartitionMismatchError, StructuralDriftError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ptap_b200.so")
+# PTAP_LIB_PATH: an A/B build of the same library (csrc/Makefile VARIANT=...)
+LIB_PATH = os.environ.get("PTAP_LIB_PATH") or os.path.join(_HERE, "_ptap_b200.so")
 
 c_i64 = ctypes.c_int64
 c_p = ctypes.c_void_p

@@ -1186,6 +1186,8 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   uint2 *fold = nullptr;
   uint32_t *outer = nullptr;
   CKS(palloc(p, &fold, (int64_t)h[1] + 8, CAT_PLAN, st));
+  CK(cudaMemsetAsync(fold + h[1], 0, 8 * sizeof(uint2), st));
+  l.fold_zero = (uint32_t)h[1];
   CKS(palloc(p, &outer, (int64_t)h[2] + 32, CAT_PLAN, st));
   l.fold = fold; l.outer = outer;
   CK(launch_lock_programs(ncls, op, plen8, p->maps, reps, ltab, cls, fold, outer, st));

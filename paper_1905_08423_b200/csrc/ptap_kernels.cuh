@@ -259,12 +259,13 @@ struct __align__(16) LockClass {  // one structural class of fine rows (32 bytes
 };
 struct LockArgs {
   int32_t nloc, ntiles, acap, aps;  // acap: staged A entries per tile, aps: AP buffer stride (doubles, odd)
+  uint32_t fold_zero;               // index of eight zero entries behind the fold programs
   const uint32_t *pq;       // [nloc] Q index of the first entry of P row k
   double *Q;                // [nnz(P_d)] P's values, class-major (rewritten every pass)
   const int32_t *cbQ;       // [nnz(P_d)] C row start of every P entry, same order
   const uint32_t *rowinfo;  // [nloc] per tile, rows sorted by class: class << 8 | row - tile start
   const LockClass *cls;
-  const uint2 *fold;        // x: A entry*8 | A entry*4 << 8 | valid << 30 | last-of-slot << 31, y: Q offset of the P entry
+  const uint2 *fold;        // x: A entry*8 | last-of-slot << 15 | A entry*4 << 16, y: Q offset of the P entry
   const uint32_t *outer;    // slot*8 | target << 8 | position in the C row << 16
   const int32_t *ltab;      // [0, NLEN) rows of P per length, [NLEN, 2 NLEN) first Q index per length
 };

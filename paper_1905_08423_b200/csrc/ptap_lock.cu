@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     aval[cend - c0 + tid] = __ldg(op.ad_val + cend + tid);
   }
   if (tid <= r1 - r0) rs[tid] = (int32_t)(__ldg(op.ad_rp + r0 + tid) - c0);
+  if (tid == 0) rs[LT + 2] = 0;
   // the lane's row (sorted position 32 g + lane of the tile) and its class
   const int cnt = min(32, r1 - r0 - 32 * g);
   const bool active = lane < cnt;
@@ -186,77 +187,108 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
   lk_group_bar(g);
 
   // fold, slot-major: warp w folds the slots of its range of the lane's class
-  // program; one register accumulator, stored once per slot
+  // program; one register accumulator, stored once per slot.  Entries past a
+  // lane's sub-program are zero: they read the row's first A entry and Q
+  // value and accumulate into a register that is never stored (a lane with
+  // no program reads Q[0] through a zero word of shared memory).
   {
     const int nch = sub_hi - sub_lo;
     const int nchmax = __reduce_max_sync(FULLM, nch);
     const uint2 *fp = la.fold + K_fold_off + (size_t)sub_lo * 8;
-    const uint32_t a_sa = aval_sa + (uint32_t)rsl * 8u, c_sa = acol_sa + (uint32_t)rsl * 4u;
+    const uint32_t a_sa = sub_all > 0 ? aval_sa + (uint32_t)rsl * 8u : aval_sa;
+    const uint32_t c_sa = sub_all > 0 ? acol_sa + (uint32_t)rsl * 4u : sm_u32(rs + LT + 2);
     uint32_t o_sa = ap_sa0 + (uint32_t)(lane * la.aps + slot0) * 8u;
     double acc = 0.0;
-    uint2 en[8];
+    const uint2 *zchunk = la.fold + la.fold_zero;  // eight zero entries
+    auto load = [&](uint2(&e)[8], int c) {
+      const uint4 *src = (const uint4 *)(c < nch ? fp + c * 8 : zchunk);  // chunks are 64-byte aligned
 #pragma unroll
-    for (int u = 0; u < 8; ++u) en[u] = make_uint2(0u, 0u);
-    if (nch > 0) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) en[u] = __ldg(fp + u);
-    }
-#pragma unroll 1
-    for (int c = 0; c < nchmax; ++c) {
-      uint2 e[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) e[u] = en[u];
-      if (c + 1 < nch) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) en[u] = __ldg(fp + (c + 1) * 8 + u);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) en[u] = make_uint2(0u, 0u);
+      for (int u = 0; u < 4; ++u) {
+        const uint4 v = __ldg(src + u);
+        e[2 * u] = make_uint2(v.x, v.y);
+        e[2 * u + 1] = make_uint2(v.z, v.w);
       }
+    };
+    auto process = [&](const uint2(&e)[8]) {
       double av[8], pv[8];
       uint32_t qi[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         av[u] = lk_lds_f64(a_sa + (e[u].x & 0xffu));
-        qi[u] = lk_lds_u32(c_sa + ((e[u].x >> 8) & 0x7fu));
+        qi[u] = lk_lds_u32(c_sa + (e[u].x >> 16));
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) pv[u] = (e[u].x & 0x40000000u) ? __ldg(la.Q + ((size_t)qi[u] + e[u].y)) : 0.0;
+      for (int u = 0; u < 8; ++u) pv[u] = __ldg(la.Q + (qi[u] + e[u].y));
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (e[u].x & 0x40000000u) acc = fma(av[u], pv[u], acc);
-        if (e[u].x & 0x80000000u) {
+        acc = fma(av[u], pv[u], acc);
+        if (e[u].x & 0x8000u) {
           lk_sts_f64(o_sa, acc);
           o_sa += 8u;
           acc = 0.0;
         }
+      }
+    };
+    // two chunks per round, the next chunk's entries loaded while one folds
+    uint2 ea[8], eb[8];
+    load(ea, 0);
+#pragma unroll 1
+    for (int c = 0; c < nchmax; c += 2) {
+      load(eb, c + 1);
+      process(ea);
+      if (c + 1 < nchmax) {
+        load(ea, c + 2);
+        process(eb);
       }
     }
   }
   lk_group_bar(g);
 
   // outer products, transposed: the lanes take the (target, slot) items of
-  // row r's class; warp w takes rows w, w + LW, ...
+  // row r's class; warp w takes rows w, w + LW, ...  The decoded program words
+  // of the first two rounds stay in registers while the class does not change.
   {
     const uint32_t rstride = (uint32_t)la.aps * 8u;
-    uint32_t cached = 0xffffffffu, wd0 = 0xffffffffu, wd1 = 0xffffffffu;
+    uint32_t cached = 0xffffffffu;
+    uint32_t s0a = 0, tv0 = 0, tc0 = 0, ps0 = 0, s1a = 0, tv1 = 0, tc1 = 0, ps1 = 0;
+    bool ok0 = false, ok1 = false;
     for (int r = w; r < cnt; r += LW) {
       const uint32_t off = __shfl_sync(FULLM, K_outer_off, r);
       const int nit = __shfl_sync(FULLM, K_niter, r);
       if (off != cached) {
-        wd0 = nit > 0 ? __ldg(la.outer + off + lane) : 0xffffffffu;
-        wd1 = nit > 1 ? __ldg(la.outer + off + 32 + lane) : 0xffffffffu;
+        const uint32_t wd0 = nit > 0 ? __ldg(la.outer + off + lane) : 0xffffffffu;
+        const uint32_t wd1 = nit > 1 ? __ldg(la.outer + off + 32 + lane) : 0xffffffffu;
+        ok0 = wd0 != 0xffffffffu;
+        ok1 = wd1 != 0xffffffffu;
+        s0a = ap_sa0 + (wd0 & 0xffu);
+        tv0 = tgv_sa + ((wd0 >> 8) & 0xffu) * (TGS * 8u);
+        tc0 = tgc_sa + ((wd0 >> 8) & 0xffu) * (TGS * 4u);
+        ps0 = wd0 >> 16;
+        s1a = ap_sa0 + (wd1 & 0xffu);
+        tv1 = tgv_sa + ((wd1 >> 8) & 0xffu) * (TGS * 8u);
+        tc1 = tgc_sa + ((wd1 >> 8) & 0xffu) * (TGS * 4u);
+        ps1 = wd1 >> 16;
         cached = off;
       }
-      const uint32_t apr = ap_sa0 + (uint32_t)r * rstride;
-      for (int u = 0; u < nit; ++u) {
-        const uint32_t wd = u == 0 ? wd0 : (u == 1 ? wd1 : __ldg(la.outer + off + u * 32 + lane));
+      const uint32_t ro = (uint32_t)r * rstride, r8 = (uint32_t)r * 8u, r4 = (uint32_t)r * 4u;
+      if (ok0) {
+        const double apv = lk_lds_f64(s0a + ro), tv = lk_lds_f64(tv0 + r8);
+        const uint32_t cb = lk_lds_u32(tc0 + r4);
+        atomicAdd(c_val + (cb + ps0), tv * apv);
+      }
+      if (ok1) {
+        const double apv = lk_lds_f64(s1a + ro), tv = lk_lds_f64(tv1 + r8);
+        const uint32_t cb = lk_lds_u32(tc1 + r4);
+        atomicAdd(c_val + (cb + ps1), tv * apv);
+      }
+      for (int u = 2; u < nit; ++u) {
+        const uint32_t wd = __ldg(la.outer + off + u * 32 + lane);
         if (wd != 0xffffffffu) {
-          const uint32_t s8 = wd & 0xffu, jt = (wd >> 8) & 0xffu, pos = wd >> 16;
-          const double apv = lk_lds_f64(apr + s8);
-          const double tv = lk_lds_f64(tgv_sa + (jt * TGS + (uint32_t)r) * 8u);
-          const uint32_t cb = lk_lds_u32(tgc_sa + (jt * TGS + (uint32_t)r) * 4u);
-          atomicAdd(c_val + ((size_t)cb + pos), tv * apv);
+          const uint32_t jt = (wd >> 8) & 0xffu;
+          const double apv = lk_lds_f64(ap_sa0 + ro + (wd & 0xffu));
+          const double tv = lk_lds_f64(tgv_sa + jt * (TGS * 8u) + r8);
+          const uint32_t cb = lk_lds_u32(tgc_sa + jt * (TGS * 4u) + r4);
+          atomicAdd(c_val + (cb + (wd >> 16)), tv * apv);
         }
       }
     }
@@ -625,8 +657,8 @@ __global__ void __launch_bounds__(128) k_lock_programs(int ncls, Ops op, const u
     for (int t = 0; t < L; ++t) {
       const int s = sm[p++] & 0x1f;
       const int at = pos[s]++;
-      const uint32_t last = at + 1 == cnt[s] ? 0x80000000u : 0u;
-      fp[at] = make_uint2((uint32_t)(j * 8) | ((uint32_t)(j * 4) << 8) | 0x40000000u | last, (uint32_t)t * N);
+      const uint32_t last = at + 1 == cnt[s] ? 0x8000u : 0u;
+      fp[at] = make_uint2((uint32_t)(j * 8) | ((uint32_t)(j * 4) << 16) | last, (uint32_t)t * N);
     }
   }
   uint32_t *ow = outer + K.outer_off;

@@ -396,7 +396,7 @@ def _remote_csr(rr: RemoteRows, m: int, device) -> DeviceCsr:
 
 
 def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str, deterministic=None,
-              maps=None) -> TripleProductPlan:
+              maps=None, lockstep=None) -> TripleProductPlan:
     _check_triple_operands(a, p)
     L = _lib.load()
     torch = _torch()
@@ -424,6 +424,8 @@ def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str, de
             _lib.check(L.ptap_plan_set_option(plan._h, b"deterministic", 1), "plan option")
         if maps is not None:
             _lib.check(L.ptap_plan_set_option(plan._h, b"maps", 1 if maps else 0), "plan option")
+        if lockstep is not None:
+            _lib.check(L.ptap_plan_set_option(plan._h, b"lockstep", 1 if lockstep else 0), "plan option")
         stream = _stream_ptr()
         _lib.check(L.ptap_symbolic_send(plan._h, ctypes.byref(st), stream), "symbolic send")
         s_rows, s_rp, s_col, _ = plan._staging_device()
@@ -598,12 +600,12 @@ def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankCon
     return plan.c_local() if to_host else plan.c_device()
 
 
-def aao_symbolic(a, p, ctx, *, deterministic=None, maps=None) -> TripleProductPlan:
+def aao_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
     """All-at-once symbolic: send loop, exchange, local loop (Alg. 7).
     ``deterministic=True`` (or PTAP_DETERMINISTIC=1) selects the
     owner-computes numeric kernel: bitwise-repeatable passes whose C is
     bit-identical to the reference's at one rank."""
-    return _symbolic(a, p, ctx, ALL_AT_ONCE, deterministic, maps)
+    return _symbolic(a, p, ctx, ALL_AT_ONCE, deterministic, maps, lockstep)
 
 
 def aao_numeric(a, p, plan, ctx):
@@ -611,19 +613,19 @@ def aao_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, ALL_AT_ONCE)
 
 
-def merged_symbolic(a, p, ctx, *, deterministic=None, maps=None) -> TripleProductPlan:
+def merged_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
     """Merged all-at-once: one fused loop computes each AP row once (Alg. 9)."""
-    return _symbolic(a, p, ctx, MERGED, deterministic, maps)
+    return _symbolic(a, p, ctx, MERGED, deterministic, maps, lockstep)
 
 
 def merged_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, MERGED)
 
 
-def two_step_symbolic(a, p, ctx, *, deterministic=None, maps=None) -> TripleProductPlan:
+def two_step_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
     """Two-step: C~ = A P, explicit P^T, then P^T C~ (Alg. 5); always
     deterministic (every entry is folded in the reference's order)."""
-    return _symbolic(a, p, ctx, TWO_STEP, deterministic, maps)
+    return _symbolic(a, p, ctx, TWO_STEP, deterministic, maps, lockstep)
 
 
 def two_step_numeric(a, p, plan, ctx):
@@ -634,15 +636,17 @@ _SYMBOLIC = {TWO_STEP: two_step_symbolic, ALL_AT_ONCE: aao_symbolic, MERGED: mer
 _NUMERIC = {TWO_STEP: two_step_numeric, ALL_AT_ONCE: aao_numeric, MERGED: merged_numeric}
 
 
-def run_symbolic(a, p, algorithm: str, ctx, *, deterministic=None, maps=None) -> TripleProductPlan:
+def run_symbolic(a, p, algorithm: str, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
     """Symbolic phase (reference run_symbolic, src/tripleproduct.py:499-502).
     Options beyond the reference: ``deterministic`` (bitwise-repeatable
     numeric passes, bit-identical to the reference at one rank) and ``maps``
     (None: keep plan maps when rows repeat; False: hash numeric path, nothing
-    stored per row; True: always keep maps)."""
+    stored per row; True: always keep maps) and ``lockstep`` (None/True: the
+    class-lockstep numeric kernel when the plan is eligible, numeric_path 3;
+    False: the per-row mapped kernels)."""
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
-    return _SYMBOLIC[algorithm](a, p, ctx, deterministic=deterministic, maps=maps)
+    return _SYMBOLIC[algorithm](a, p, ctx, deterministic=deterministic, maps=maps, lockstep=lockstep)
 
 
 def run_numeric(a, p, plan: TripleProductPlan, ctx):

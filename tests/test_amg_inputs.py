@@ -109,12 +109,13 @@ def test_map_policy_structured_vs_unstructured(cfg5_large):
 
     ctx = pk.single_rank_context()
     A3, P3 = gen.config_operands(gen.CONFIGS["cfg3"], n_fine=24)
-    for (A, P), path in (((A3, P3), 1), (cfg5_large, 0)):
+    # numeric_path: 3 = plan maps run by the class-lockstep kernel, 1 = plan maps, 0 = hash tables
+    for (A, P), paths in (((A3, P3), (1, 3)), (cfg5_large, (0,))):
         a, p = pk.distribute(A, P, 1, 0)
         plan = pk.run_symbolic(a, p, "allatonce", ctx)
         d = plan.device_counters()
-        assert d["numeric_path"] == path, d
-        assert (d["map_bytes"] > 0) == (path == 1)
+        assert d["numeric_path"] in paths, d
+        assert (d["map_bytes"] > 0) == (0 not in paths)
         assert 0 <= d["row_structures_ppm"] <= 10 ** 6
     A, P = cfg5_large
     want = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values, P.row_offsets,
