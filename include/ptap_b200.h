@@ -166,8 +166,18 @@ ptap_status ptap_plan_destroy(ptap_plan *plan);
  *     32 rows of one structural class in lockstep, A tiles staged by TMA,
  *     P's values class-major) for plans with maps and one-rank structure:
  *     -1/1 (default) when the plan is eligible, 0 never (the per-row mapped
- *     kernels run instead).  counters.numeric_path == 3 when it is in use. */
+ *     kernels run instead).  counters.numeric_path == 3 when it is in use.
+ *   "single_shot" (0/1): symbolic and numeric in one pass (BASELINE north_star
+ *     (3); SURVEY 3.2's additional single-shot fast path): when the rank neither
+ *     sends nor receives, ptap_symbolic_local walks A's rows once, computing
+ *     every AP row with values and adding its outer products, keys and values
+ *     together, into the C arena, which is drained into sorted CSR with the
+ *     values as payload; C then holds the product of the symbolic-time operands
+ *     (ptap_plan_values_ready) and no numeric call is needed.  No maps are
+ *     kept: later numeric passes on the plan run the hash path. */
 ptap_status ptap_plan_set_option(ptap_plan *plan, const char *key, int64_t value);
+/* 1 when the last symbolic phase also computed C's values (single_shot). */
+ptap_status ptap_plan_values_ready(ptap_plan *plan, int *ready);
 
 /* Symbolic, phase 1: AP-row binning and the send-side structure C_s (all
  * variants), plus (two-step) C~ and the local transposes. */

@@ -67,6 +67,7 @@ _EXPORTS = {
     "ptap_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(Operands), ctypes.POINTER(c_p)]),
     "ptap_plan_destroy": (ctypes.c_int, [c_p]),
     "ptap_plan_set_option": (ctypes.c_int, [c_p, ctypes.c_char_p, c_i64]),
+    "ptap_plan_values_ready": (ctypes.c_int, [c_p, ctypes.POINTER(ctypes.c_int)]),
     "ptap_symbolic_send": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), c_p]),
     "ptap_plan_staging": (ctypes.c_int, [c_p, ctypes.POINTER(Staging)]),
     "ptap_symbolic_local": (ctypes.c_int, [c_p, ctypes.POINTER(Operands), ctypes.POINTER(Received), c_p]),

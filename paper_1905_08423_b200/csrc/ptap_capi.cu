@@ -132,6 +132,8 @@ struct ptap_plan {
   bool lock = false;                // class-lockstep numeric kernel (ptap_lock.cu) replaces q4a
   int lock_opt = -1;                // plan option "lockstep": -1 when eligible, 0 never, 1 same as -1
   int lock_classes = 0;
+  bool single_shot = false;         // plan option: symbolic_local also computes C's values (one pass over A)
+  bool values_ready = false;        // ... and did: C holds the product of the symbolic-time operands
   int64_t max_nap = 0;              // widest AP row
   int64_t qmap_bytes = 0;           // tile gather maps (interned)
   bool smap_deferred = false;       // slot-map buffer not allocated yet (chunked or allocated on first use)
@@ -510,8 +512,11 @@ ptap_status arena_grow(ptap_plan *p, Arena &ar, cudaStream_t st) {
 }
 
 // Arena -> CSR over `nrows_dense` rows (row id = key / m), columns sorted.
+// avals / val_out: the single-shot pass's value array beside the keys, drained
+// as the sort's payload into the rows' values
 ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, int64_t **rp_out, int32_t **col_out,
-                         int64_t *nnz_out, int64_t **cnt_keep, cudaStream_t st) {
+                         int64_t *nnz_out, int64_t **cnt_keep, cudaStream_t st, const double *avals = nullptr,
+                         double **val_out = nullptr) {
   int64_t *cnt = nullptr, *rp = nullptr, *scratch = nullptr;
   Tracer tr;
   tr.on = tr.on && getenv("PTAP_TRACE")[0] == '2';
@@ -532,19 +537,26 @@ ptap_status arena_to_csr(ptap_plan *p, Arena ar, int64_t nrows_dense, int cat, i
   pfree(p, scratch, st);
   CKS(palloc(p, &cursor, nrows_dense, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(cursor, 0, sizeof(int64_t) * (nrows_dense > 0 ? nrows_dense : 1), st));
-  CK(launch_arena_scatter(ar, p->m, rp, cursor, col, st));
+  int64_t *payload = nullptr;
+  if (avals) {
+    CKS(palloc(p, &payload, nnz, cat, st));
+    CK(launch_arena_scatter_vals(ar, p->m, rp, cursor, col, avals, payload, st));
+  } else {
+    CK(launch_arena_scatter(ar, p->m, rp, cursor, col, st));
+  }
   pfree(p, cursor, st);
   tr.mark(st, "  drain: scatter");
   int32_t *wide = nullptr;
   CKS(palloc(p, &wide, nnz / 1024 + 2, CAT_TRANSIENT, st));
   CK(cudaMemsetAsync(p->d_u64 + 6, 0, sizeof(unsigned long long), st));
-  CK(launch_sort_rows(nrows_dense, rp, col, nullptr, wide, p->d_u64 + 6, st));
+  CK(launch_sort_rows(nrows_dense, rp, col, payload, wide, p->d_u64 + 6, st));
   unsigned long long nwide = 0;
   CK(cudaMemcpyAsync(&nwide, p->d_u64 + 6, sizeof(nwide), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   tr.mark(st, "  drain: sort rows");
-  CK(launch_sort_rows_block((int64_t)nwide, wide, rp, col, nullptr, p->d_status, st));
+  CK(launch_sort_rows_block((int64_t)nwide, wide, rp, col, payload, p->d_status, st));
   tr.mark(st, "  drain: sort wide");
+  if (val_out) *val_out = (double *)payload;  // the payload holds the doubles' bits
   pfree(p, wide, st);
   p->cnt.kernel_launches += 6;
   if (cnt_keep) *cnt_keep = cnt; else pfree(p, cnt, st);
@@ -1704,6 +1716,11 @@ ptap_status ptap_plan_set_option(ptap_plan *p, const char *key, int64_t value) {
     p->deterministic = value != 0;
     return PTAP_OK;
   }
+  if (!strcmp(key, "single_shot")) {
+    p->single_shot = value != 0;
+    if (p->single_shot) p->maps_opt = 0;  // nothing kept per row: later passes run the hash numeric path
+    return PTAP_OK;
+  }
   if (!strcmp(key, "lockstep")) {
     p->lock_opt = value < 0 ? -1 : (value ? 1 : 0);
     return PTAP_OK;
@@ -1713,6 +1730,12 @@ ptap_status ptap_plan_set_option(ptap_plan *p, const char *key, int64_t value) {
     return PTAP_OK;
   }
   return fail(PTAP_ERR_VALUE, std::string("unknown plan option '") + key + "'");
+}
+
+ptap_status ptap_plan_values_ready(ptap_plan *p, int *ready) {
+  if (!p || !ready) return fail(PTAP_ERR_VALUE, "null argument");
+  *ready = p->values_ready ? 1 : 0;
+  return PTAP_OK;
 }
 
 ptap_status ptap_plan_destroy(ptap_plan *p) {
@@ -1880,6 +1903,40 @@ ptap_status ptap_symbolic_local(ptap_plan *p, const ptap_operands *ops, const pt
   if (p->alg != PTAP_MERGED || p->merged_deferred)
     CKS(arena_alloc(p, p->local_arena, local_arena_estimate(p, rnnz), st, (unsigned long long)p->ncl));
   tr.mark(st, "local arena alloc");
+  // single-shot: the same arena takes keys and values in one pass over A
+  p->values_ready = false;
+  if (p->single_shot && local_loop_here && !p->want_maps && !(recv && recv->nrows > 0) && ops->p_off.nnz == 0) {
+    Arena &la = p->local_arena;
+    double *avals = nullptr;
+    for (int attempt = 0;; ++attempt) {
+      if (attempt >= 8) return fail(PTAP_ERR_OOM, "single-shot arena kept overflowing");
+      CKS(palloc(p, &avals, (int64_t)(la.mask + 1), CAT_TRANSIENT, st));
+      CK(cudaMemsetAsync(avals, 0, sizeof(double) * (la.mask + 1), st));
+      CKS(for_bins(p, p->bins_local, [&](const LaunchShape &s, const int32_t *rows, unsigned long long n) {
+        return launch_outer_oneshot(s, op, rows, n, la, avals, p->d_status, st);
+      }));
+      int s = 0;
+      CKS(read_status(p, st, &s));
+      if (!(s & ST_ARENA_FULL)) {
+        if (s) return status_to_error(s, "single-shot pass");
+        break;
+      }
+      pfree(p, avals, st);  // a grown arena keeps the keys; the values are recomputed
+      CKS(arena_grow(p, la, st));
+    }
+    p->cnt.symbolic_row_kernel_calls += p->bins_local.selected;
+    p->cnt.numeric_row_kernel_calls += p->bins_local.selected;
+    p->r_src_nnz_off.clear();
+    p->r_nnz = 0;
+    tr.mark(st, "single-shot outer pass");
+    CKS(arena_to_csr(p, la, p->ncl, CAT_OUTPUT, &p->c_rp, &p->c_col, &p->c_nnz, nullptr, st, avals, &p->c_val));
+    tr.mark(st, "C drain + sort (values)");
+    pfree(p, avals, st);
+    pfree(p, la.keys, st);
+    la = Arena{nullptr, 0};
+    p->values_ready = true;
+    goto c_allocated;
+  }
   {
   Arena &la = p->local_arena;
   if (local_loop_here) {
@@ -1942,8 +1999,10 @@ c_allocated:
   tr.mark(st, "position maps");
   CKS(build_q4a_runs(p, op, ops, st));
   // C's values last: the position maps' transient peak is over by now
-  CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
-  CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
+  if (!p->values_ready) {
+    CKS(palloc(p, &p->c_val, p->c_nnz, CAT_OUTPUT, st));
+    CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * (p->c_nnz > 0 ? p->c_nnz : 1), st));
+  }
   if (p->rows_unstructured && !(p->alg != PTAP_TWO_STEP && p->mapped) && !getenv("PTAP_NO_ROW_ORDER")) {
     // an operator whose rows do not repeat: visit rows in aggregate order
     // (k_row_order_keys) -- the hash numeric path, and two-step's C~ = A P

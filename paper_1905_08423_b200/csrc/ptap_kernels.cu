@@ -271,6 +271,84 @@ __device__ __forceinline__ void arena_insert(const Arena &a, unsigned long long 
   atomicOr(status, ST_ARENA_FULL);
 }
 
+// The same insertion returning the key's slot (single-shot pass: the slot
+// indexes a value array beside the keys); ~0 when the arena is full.
+__device__ __forceinline__ unsigned long long arena_insert_slot(const Arena &a, unsigned long long row,
+                                                                unsigned long long col, int *status) {
+  const unsigned long long key = row * a.m + col;
+  unsigned long long *ar = a.keys;
+  if (a.log2b > 0) {
+    const unsigned long long bm = (1ull << a.log2b) - 1ull;
+    const unsigned long long b0 = (row << a.log2b) & a.mask;
+    unsigned long long o = (unsigned long long)hash32((uint32_t)col, a.log2b) & bm;
+    for (unsigned long long probe = 0; probe <= bm; ++probe) {
+      const unsigned long long hh = b0 | o;
+      const unsigned long long k = ar[hh];
+      if (k == key) return hh;
+      if (k == EMPTY64) {
+        const unsigned long long old = atomicCAS(ar + hh, EMPTY64, key);
+        if (old == EMPTY64 || old == key) return hh;
+      }
+      o = (o + 1) & bm;
+    }
+  }
+  unsigned long long h = hash64(key) & a.mask;
+  for (int probe = 0; probe < 8192; ++probe) {
+    unsigned long long k = ar[h];
+    if (k == key) return h;
+    if (k == EMPTY64) {
+      unsigned long long old = atomicCAS(ar + h, EMPTY64, key);
+      if (old == EMPTY64 || old == key) return h;
+    }
+    h = (h + 1) & a.mask;
+  }
+  atomicOr(status, ST_ARENA_FULL);
+  return ~0ull;
+}
+
+// Single-shot pass: symbolic and numeric together (BASELINE north_star (3);
+// SURVEY 3.2 "an additional single-shot fast path").  One walk over the fine
+// rows: AP(i,:) with values in the group's hash table (row_ap_numeric,
+// src/_kernels.py:203-227), then every outer product P(i,J) * AP(i,g) goes
+// into the local C arena, key and value at once (the key's slot indexes a
+// value array): no second pass over A, no maps.  The arena is drained into
+// sorted CSR with the values as payload (k_arena_scatter_vals, k_sort_rows).
+template <int GROUP, bool GT>
+__global__ void __launch_bounds__(256) k_outer_oneshot(Ops op, const int32_t *rows, unsigned long long nrows,
+                                                       int log2t, unsigned char *gtables, Arena local, double *avals,
+                                                       int *status) {
+  GroupTables tb = group_tables<GROUP, true, GT>(gtables, log2t);
+  const int gpw = 32 / GROUP;
+  const int gpc = (blockDim.x >> 5) * gpw;
+  const int T = 1 << log2t;
+  const int gl = lane_id() & (GROUP - 1);
+  for (unsigned long long r0 = (unsigned long long)blockIdx.x * gpc + (threadIdx.x >> 5) * gpw; r0 < nrows;
+       r0 += (unsigned long long)gridDim.x * gpc) {
+    unsigned long long ridx = r0 + lane_id() / GROUP;
+    int64_t i = ridx < nrows ? (rows ? (int64_t)rows[ridx] : (int64_t)ridx) : -1;
+    int64_t pd0 = 0, pd1 = 0;
+    if (i >= 0) { pd0 = op.pd_rp[i]; pd1 = op.pd_rp[i + 1]; }
+    if (pd1 <= pd0) i = -1;
+    if (__all_sync(FULL, i < 0)) continue;
+    table_clear<GROUP>(tb.keys, T);
+    ap_row_accumulate<GROUP, true>(op, i, tb.keys, tb.vals, log2t, tb.ps, status);
+    if (i >= 0) {
+      for (int64_t jj = pd0; jj < pd1; ++jj) {
+        const unsigned long long J = (unsigned long long)__ldg(op.pd_col + jj);
+        const double pij = __ldg(op.pd_val + jj);
+        for (int s = gl; s < T; s += GROUP) {
+          const int32_t g = tb.keys[s];
+          if (g != EMPTY32) {
+            const unsigned long long slot = arena_insert_slot(local, J, (unsigned long long)g, status);
+            if (slot != ~0ull) atomicAdd(avals + slot, __dmul_rn(pij, tb.vals[s]));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // structural outer products P(i,:) (x) AP(i,:) (src/_kernels.py:361-418):
 // local rows go to the local arena keyed (J - c_lo)*m + g, send rows to the
 // send arena keyed J*m + g.
@@ -447,6 +525,18 @@ __global__ void k_arena_scatter(Arena ar, unsigned long long m, const int64_t *r
   unsigned long long r = k / m;
   unsigned long long pos = (unsigned long long)rp[r] + atomicAdd((unsigned long long *)(cursor + r), 1ull);
   col[pos] = (int32_t)(k - r * m);
+}
+
+__global__ void k_arena_scatter_vals(Arena ar, unsigned long long m, const int64_t *rp, int64_t *cursor, int32_t *col,
+                                     const double *avals, int64_t *payload) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > ar.mask) return;
+  unsigned long long k = ar.keys[s];
+  if (k == EMPTY64) return;
+  unsigned long long r = k / m;
+  unsigned long long pos = (unsigned long long)rp[r] + atomicAdd((unsigned long long *)(cursor + r), 1ull);
+  col[pos] = (int32_t)(k - r * m);
+  payload[pos] = __double_as_longlong(avals[s]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1402,6 +1492,14 @@ cudaError_t launch_outer_symbolic(const LaunchShape &s, const Ops &op, const int
                           mo, status);
 }
 
+cudaError_t launch_outer_oneshot(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                 Arena local, double *avals, int *status, cudaStream_t stream) {
+  const int group = s.group, warps = s.warps, log2t = s.log2t, max_ctas = s.max_ctas;
+  unsigned char *gtables = s.gtables;
+  cudaError_t e;
+  PTAP_ROWKERNEL_DISPATCH(k_outer_oneshot, true, op, rows, nrows, log2t, gtables, local, avals, status);
+}
+
 cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                  int do_send, int do_local, const OuterTargets &tg, int *status,
                                  cudaStream_t stream) {
@@ -1484,6 +1582,14 @@ cudaError_t launch_arena_scatter(Arena ar, int64_t m, const int64_t *rp, int64_t
                                  cudaStream_t st) {
   unsigned long long cap = ar.mask + 1;
   k_arena_scatter<<<nblk((int64_t)cap, 256), 256, 0, st>>>(ar, (unsigned long long)m, rp, cursor, col);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arena_scatter_vals(Arena ar, int64_t m, const int64_t *rp, int64_t *cursor, int32_t *col,
+                                      const double *avals, int64_t *payload, cudaStream_t st) {
+  unsigned long long cap = ar.mask + 1;
+  k_arena_scatter_vals<<<nblk((int64_t)cap, 256), 256, 0, st>>>(ar, (unsigned long long)m, rp, cursor, col, avals,
+                                                                payload);
   return cudaGetLastError();
 }
 

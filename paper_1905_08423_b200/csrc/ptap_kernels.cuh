@@ -100,6 +100,10 @@ cudaError_t launch_build_pmap(const Ops &op, unsigned long long nrows, const Map
 cudaError_t launch_outer_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                                  int do_send, int do_local, const OuterTargets &tg, int *status,
                                  cudaStream_t stream);
+cudaError_t launch_outer_oneshot(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
+                                 Arena local, double *avals, int *status, cudaStream_t stream);
+cudaError_t launch_arena_scatter_vals(Arena ar, int64_t m, const int64_t *rp, int64_t *cursor, int32_t *col,
+                                      const double *avals, int64_t *payload, cudaStream_t st);
 cudaError_t launch_ct_fill(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,
                            const int64_t *ct_rp, int32_t *ct_col, int *status, cudaStream_t stream);
 cudaError_t launch_ct_numeric(const LaunchShape &s, const Ops &op, const int32_t *rows, unsigned long long nrows,

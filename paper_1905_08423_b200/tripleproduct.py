@@ -302,6 +302,16 @@ class TripleProductPlan:
             pass
 
     @property
+    def values_ready(self) -> bool:
+        """True when the symbolic phase also computed C's values (the
+        single-shot pass): C holds the product of the symbolic-time operands."""
+        if not self._h:
+            return False
+        r = ctypes.c_int(0)
+        _lib.check(self._lib().ptap_plan_values_ready(self._h, ctypes.byref(r)), "values ready")
+        return bool(r.value)
+
+    @property
     def deterministic(self) -> bool:
         """True when repeated numeric passes are bitwise identical: the
         two-step comparator, or an all-at-once / merged plan running the
@@ -396,7 +406,7 @@ def _remote_csr(rr: RemoteRows, m: int, device) -> DeviceCsr:
 
 
 def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str, deterministic=None,
-              maps=None, lockstep=None) -> TripleProductPlan:
+              maps=None, lockstep=None, single_shot=None) -> TripleProductPlan:
     _check_triple_operands(a, p)
     L = _lib.load()
     torch = _torch()
@@ -426,6 +436,8 @@ def _symbolic(a: DistMatrix, p: DistMatrix, ctx: RankContext, algorithm: str, de
             _lib.check(L.ptap_plan_set_option(plan._h, b"maps", 1 if maps else 0), "plan option")
         if lockstep is not None:
             _lib.check(L.ptap_plan_set_option(plan._h, b"lockstep", 1 if lockstep else 0), "plan option")
+        if single_shot:
+            _lib.check(L.ptap_plan_set_option(plan._h, b"single_shot", 1), "plan option")
         stream = _stream_ptr()
         _lib.check(L.ptap_symbolic_send(plan._h, ctypes.byref(st), stream), "symbolic send")
         s_rows, s_rp, s_col, _ = plan._staging_device()
@@ -600,12 +612,12 @@ def _numeric(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx: RankCon
     return plan.c_local() if to_host else plan.c_device()
 
 
-def aao_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
+def aao_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None, single_shot=None) -> TripleProductPlan:
     """All-at-once symbolic: send loop, exchange, local loop (Alg. 7).
     ``deterministic=True`` (or PTAP_DETERMINISTIC=1) selects the
     owner-computes numeric kernel: bitwise-repeatable passes whose C is
     bit-identical to the reference's at one rank."""
-    return _symbolic(a, p, ctx, ALL_AT_ONCE, deterministic, maps, lockstep)
+    return _symbolic(a, p, ctx, ALL_AT_ONCE, deterministic, maps, lockstep, single_shot)
 
 
 def aao_numeric(a, p, plan, ctx):
@@ -613,19 +625,19 @@ def aao_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, ALL_AT_ONCE)
 
 
-def merged_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
+def merged_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None, single_shot=None) -> TripleProductPlan:
     """Merged all-at-once: one fused loop computes each AP row once (Alg. 9)."""
-    return _symbolic(a, p, ctx, MERGED, deterministic, maps, lockstep)
+    return _symbolic(a, p, ctx, MERGED, deterministic, maps, lockstep, single_shot)
 
 
 def merged_numeric(a, p, plan, ctx):
     return _numeric(a, p, plan, ctx, MERGED)
 
 
-def two_step_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
+def two_step_symbolic(a, p, ctx, *, deterministic=None, maps=None, lockstep=None, single_shot=None) -> TripleProductPlan:
     """Two-step: C~ = A P, explicit P^T, then P^T C~ (Alg. 5); always
     deterministic (every entry is folded in the reference's order)."""
-    return _symbolic(a, p, ctx, TWO_STEP, deterministic, maps, lockstep)
+    return _symbolic(a, p, ctx, TWO_STEP, deterministic, maps, lockstep, single_shot)
 
 
 def two_step_numeric(a, p, plan, ctx):
@@ -636,17 +648,22 @@ _SYMBOLIC = {TWO_STEP: two_step_symbolic, ALL_AT_ONCE: aao_symbolic, MERGED: mer
 _NUMERIC = {TWO_STEP: two_step_numeric, ALL_AT_ONCE: aao_numeric, MERGED: merged_numeric}
 
 
-def run_symbolic(a, p, algorithm: str, ctx, *, deterministic=None, maps=None, lockstep=None) -> TripleProductPlan:
+def run_symbolic(a, p, algorithm: str, ctx, *, deterministic=None, maps=None, lockstep=None,
+                 single_shot=None) -> TripleProductPlan:
     """Symbolic phase (reference run_symbolic, src/tripleproduct.py:499-502).
     Options beyond the reference: ``deterministic`` (bitwise-repeatable
     numeric passes, bit-identical to the reference at one rank) and ``maps``
     (None: keep plan maps when rows repeat; False: hash numeric path, nothing
     stored per row; True: always keep maps) and ``lockstep`` (None/True: the
     class-lockstep numeric kernel when the plan is eligible, numeric_path 3;
-    False: the per-row mapped kernels)."""
+    False: the per-row mapped kernels) and ``single_shot`` (True: when the
+    rank neither sends nor receives, the symbolic phase also computes C's
+    values in the same pass over A -- ``plan.values_ready``; nothing is kept
+    per row, later numeric passes hash)."""
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
-    return _SYMBOLIC[algorithm](a, p, ctx, deterministic=deterministic, maps=maps, lockstep=lockstep)
+    return _SYMBOLIC[algorithm](a, p, ctx, deterministic=deterministic, maps=maps, lockstep=lockstep,
+                                single_shot=single_shot)
 
 
 def run_numeric(a, p, plan: TripleProductPlan, ctx):
@@ -659,12 +676,19 @@ def run_numeric_device(a, p, plan: TripleProductPlan, ctx):
 
 
 def ptap(a: DistMatrix, p: DistMatrix, algorithm: str, ctx: RankContext, cache: str = CACHE_KEEP, *,
-         deterministic=None):
-    """One symbolic plus one numeric triple product; returns (C, plan)."""
+         deterministic=None, single_shot=False):
+    """One symbolic plus one numeric triple product; returns (C, plan).
+    ``single_shot=True`` (all-at-once / merged): symbolic and numeric in one
+    pass over A when the rank neither sends nor receives (BASELINE north_star
+    (3)); otherwise the two phases run as usual."""
     if cache not in (CACHE_KEEP, CACHE_FREE):
         raise ValueError(f"cache policy must be '{CACHE_KEEP}' or '{CACHE_FREE}'")
-    plan = run_symbolic(a, p, algorithm, ctx, deterministic=deterministic)
-    local = run_numeric(a, p, plan, ctx)
+    plan = run_symbolic(a, p, algorithm, ctx, deterministic=deterministic, single_shot=single_shot)
+    if single_shot and plan.values_ready:
+        plan._sync_counters()
+        local = plan.c_local()
+    else:
+        local = run_numeric(a, p, plan, ctx)
     if cache == CACHE_FREE:
         plan.release_cache(ctx)
     return DistMatrix(p.col_part, p.col_part, ctx.rank, local), plan
