@@ -149,6 +149,12 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# kernels of the local loop by counters.numeric_path
+NUMERIC_KERNELS = {3: "k_lock_permute + k_lock_numeric: class-lockstep, TMA-staged A tiles",
+                   2: "k_tile_numeric: deterministic owner-computes", 1: "k_outer_numeric_q4a: per-row plan maps",
+                   0: "k_outer_numeric: hash tables"}
+
+
 def ncu_traffic():
     """dram bytes per launch of the fused numeric kernel from the committed
     ncu --set full summary (stamped with the capture it came from)."""
@@ -532,8 +538,11 @@ def our_arm(args):
         # allatonce_hash: the same algorithm without plan maps (hash tables in
         # every pass, nothing stored per row) -- the like-for-like comparator of
         # two-step, which also probes hash tables every pass
+        # allatonce_per_row: the plan maps run by the per-row mapped kernels
+        # (k_outer_numeric_q4a) instead of the class-lockstep kernel
         for name, alg, kw in (("merged", "merged", {}), ("two-step", "two-step", {}),
                               ("allatonce_deterministic", "allatonce", {"deterministic": True}),
+                              ("allatonce_per_row", "allatonce", {"lockstep": False}),
                               ("allatonce_hash", "allatonce", {"maps": False})):
             vplan, vcold, vsym, vall = warm_symbolic(alg, nwarm=3, **kw)
             vms, vkern, _ = time_numeric(pk, a, p, vplan, ctx, max(3, args.steps // 2), 2, torch)
@@ -548,13 +557,41 @@ def our_arm(args):
                          "row_scaled_diff_vs_allatonce": diff,
                          "numeric_path": vplan.device_counters()["numeric_path"],
                          "deterministic": vplan.deterministic, "memory": vmem}
-            if name in ("allatonce_deterministic", "allatonce_hash"):
+            if name in ("allatonce_deterministic", "allatonce_hash", "allatonce_per_row"):
                 out[name]["gflops"] = flops / (vms * 1e-3) / 1e9
             if name == "allatonce_deterministic" and ctx.nranks == 1:
                 det_val = vval.cpu().numpy()
             del vplan, vrp, vval
             gc.collect()
             torch.cuda.synchronize()
+
+    # --- single-shot: symbolic and numeric in one pass over A (north_star (3)),
+    # against one symbolic + one numeric phase of the default plan
+    single = None
+    if not args.no_variants and ctx.nranks == 1:
+        try:
+            ts = []
+            ok = None
+            for _ in range(4):
+                gc.collect()
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                splan = pk.run_symbolic(a, p, "allatonce", ctx, single_shot=True)
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t)
+                ok = splan.values_ready
+                srp, _, sval = splan.c_device()
+                sdiff = row_scaled_diff(c_rp_ref, c_val_ref, srp, sval, torch)
+                smem = splan.memory()
+                del splan, srp, sval
+            single = {"wall_ms": statistics.median(ts[1:]) * 1e3, "runs_ms": [t * 1e3 for t in ts],
+                      "values_ready": bool(ok), "row_scaled_diff_vs_allatonce": sdiff,
+                      "two_phase_wall_ms": out["allatonce"]["ptap_wall_ms"],
+                      "product_peak_bytes": smem["product_peak"],
+                      "what": "run_symbolic(single_shot=True): C's pattern and values from one walk over A "
+                              "(arena keys + values, drained sorted); no plan maps kept"}
+        except Exception as exc:
+            single = {"error": repr(exc)}
 
     # --- CPU baseline (rank 0, N = 1): the oracle port on the SAME full
     # workload, 1 thread, R = 1; its C doubles as the full-size parity check
@@ -614,7 +651,8 @@ def our_arm(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "traffic_source": (ncu_meta or {}).get("source"),
-                         "kernel": "ptap_numeric_local launches (k_outer_numeric_q4a)", "kernel_ms": kms,
+                         "kernel": "ptap_numeric_local launches (%s)" % NUMERIC_KERNELS.get(
+                             int(out["allatonce"]["numeric_path"]), "?"), "kernel_ms": kms,
                          "alg_bytes_per_launch": my_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -623,6 +661,7 @@ def our_arm(args):
             "variants": {k: {kk: vv for kk, vv in v.items() if kk != "memory"} for k, v in out.items()},
             "memory_bytes": {k: v["memory"] for k, v in out.items()},
             "level2": level2,
+            "single_shot": single,
             "parity_full_size": parity,
             "reference_numba": numba_leg,
             "nvlink": nvlink,

@@ -1,14 +1,16 @@
 """Summarise an ncu report of a numeric kernel: per-row instruction and L1
 wavefront budget, plus the top stall/wavefront SASS lines.
-usage: python tools/ncu_summ.py report.ncu-rep [rows]"""
+usage: python tools/ncu_summ.py report.ncu-rep [rows] [--kernel REGEX] [--write DESC OUT.txt]
+(--kernel picks one kernel of a report that holds several)"""
 import csv, io, os, subprocess, sys
 
 rep = sys.argv[1]
-nrows = float(sys.argv[2]) if len(sys.argv) > 2 else 256.0 ** 3
+nrows = float(sys.argv[2]) if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else 256.0 ** 3
+KSEL = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
 
 
 def run(*a):
-    return subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *KSEL, *a], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
@@ -29,14 +31,14 @@ for k in want:
     except ValueError:
         print(f"{k:70s} {v}")
 src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
-hdr = src[1]; data = src[2:]
+hdr = src[1]; data = [r for r in src[2:] if len(r) == len(hdr) and r != hdr]
 ix = {h: i for i, h in enumerate(hdr)}
 
 
 def f(r, k):
     try:
         return float(r[ix[k]].replace(",", ""))
-    except (ValueError, KeyError):
+    except (ValueError, KeyError, IndexError):
         return 0.0
 
 
@@ -53,7 +55,7 @@ def write_summary(rep_path, kernel_desc, out_json, out_txt, nrows_):
     """profiles/ncu_numeric_summary.json (read by bench.py for roofline.traffic)
     and a text summary of the same capture."""
     import json as _json
-    raw_ = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"],
+    raw_ = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep_path, *KSEL, "--page", "raw", "--csv"],
                                                       capture_output=True, text=True).stdout)))
     R_ = dict(zip(raw_[0], raw_[2]))
     U_ = dict(zip(raw_[0], raw_[1]))
@@ -85,6 +87,7 @@ def write_summary(rep_path, kernel_desc, out_json, out_txt, nrows_):
     return d
 
 
-if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "--write":
+if __name__ == "__main__" and "--write" in sys.argv:
     import os
-    write_summary(rep, sys.argv[4], "profiles/ncu_numeric_summary.json", sys.argv[5], nrows)
+    w = sys.argv.index("--write")
+    write_summary(rep, sys.argv[w + 1], "profiles/ncu_numeric_summary.json", sys.argv[w + 2], nrows)
