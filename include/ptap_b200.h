@@ -271,6 +271,31 @@ ptap_status ptap_gen_trilinear_fill(int64_t nc, int64_t row_lo, int64_t row_hi,
                                     const int64_t *row_ptr, int32_t *col, double *val,
                                     void *stream);
 
+/* Config 4 (block transport, problems_amg.block_transport): nn^3 nodes x ncomp
+ * components, 7-point coupling per component plus a dense in-node block;
+ * P = (I - omega D^-1 A) P_tent over agg^3 node aggregates with scipy's
+ * operation order (bit-identical to the host generator for the same omega).
+ * row_ptr of A and P first, then A, then (omega from the caller's power
+ * iteration, ptap_gen_spmv_dinv: w = D^-1 A v) P from A's values. */
+ptap_status ptap_gen_block_transport_rowptr(int64_t nn, int ncomp, int64_t agg, int64_t row_lo, int64_t row_hi,
+                                            int64_t *a_row_ptr, int64_t *a_nnz_out, int64_t *p_row_ptr,
+                                            int64_t *p_nnz_out, void *stream);
+ptap_status ptap_gen_block_transport_a(int64_t nn, int ncomp, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                                       const int64_t *row_ptr, int32_t *col, double *val, void *stream);
+ptap_status ptap_gen_spmv_dinv(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
+                               const double *v, double *w, void *stream);
+ptap_status ptap_gen_block_transport_p(int64_t nn, int ncomp, int64_t agg, double omega, int64_t row_lo,
+                                       int64_t row_hi, const int64_t *a_row_ptr, const double *a_val,
+                                       const int64_t *p_row_ptr, int32_t *p_col, double *p_val, void *stream);
+
+/* Config 5 (problems_amg.knn_laplacian): the K nearest neighbours (K <= 32) of
+ * n points of the unit cube, given sorted by cell of a G^3 grid with the
+ * cells' offsets (G^3 + 1); neighbours in sorted-index space, ascending
+ * squared distance.  The rest of the generator (symmetrised graph, greedy
+ * distance-2 aggregation, smoothed P) is device tensor plumbing in devgen.py. */
+ptap_status ptap_gen_knn(int64_t n, const double *pts, const int64_t *cell_start, int G, int K,
+                         int32_t *out_idx, double *out_d2, void *stream);
+
 /* Device L2 flush helper for benchmarking (writes a buffer larger than L2). */
 ptap_status ptap_l2_flush(void *stream);
 

@@ -97,6 +97,14 @@ _EXPORTS = {
                                              c_i64, c_p, c_p, c_p, c_p]),
     "ptap_gen_trilinear_rowptr": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, ctypes.POINTER(c_i64), c_p]),
     "ptap_gen_trilinear_fill": (ctypes.c_int, [c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p]),
+    "ptap_gen_block_transport_rowptr": (ctypes.c_int, [c_i64, ctypes.c_int, c_i64, c_i64, c_i64, c_p,
+                                                       ctypes.POINTER(c_i64), c_p, ctypes.POINTER(c_i64), c_p]),
+    "ptap_gen_block_transport_a": (ctypes.c_int, [c_i64, ctypes.c_int, ctypes.c_uint64, c_i64, c_i64, c_p, c_p,
+                                                  c_p, c_p]),
+    "ptap_gen_spmv_dinv": (ctypes.c_int, [c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "ptap_gen_block_transport_p": (ctypes.c_int, [c_i64, ctypes.c_int, c_i64, ctypes.c_double, c_i64, c_i64, c_p,
+                                                  c_p, c_p, c_p, c_p, c_p]),
+    "ptap_gen_knn": (ctypes.c_int, [c_i64, c_p, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p]),
     "ptap_l2_flush": (ctypes.c_int, [c_p]),
 }
 

@@ -53,6 +53,17 @@ def upload(A, P, dev):
     return DistMatrix(rp_a, rp_a, 0, up(A)), DistMatrix(rp_a, rp_p, 0, up(P))
 
 
+def host_copy(a, p):
+    """Host CsrMatrix copies of single-rank device operands (oracle input)."""
+    from paper_1905_08423_b200.sparse import CsrMatrix
+
+    def down(d):
+        return CsrMatrix(d.nrows, d.ncols, d.row_ptr.cpu().numpy(), d.col.cpu().numpy().astype(np.int64),
+                         d.val.cpu().numpy(), check=False)
+
+    return down(a.local.diag), down(p.local.diag)
+
+
 def csr_bytes(d):
     return d.row_ptr.numel() * 8 + d.nnz * 12
 
@@ -177,15 +188,17 @@ def main():
                            devgen.split_rows_device(prp, pcol, pval, 0, m1, 0, 64 ** 3, 64 ** 3))
             desc = "cfg3 level 2: A2 = C1 (128^3, 27-pt Galerkin), trilinear to 64^3"
         elif name == "cfg4":
-            from paper_1905_08423_b200 import problems_amg as amg
-            host = amg.block_transport(args.cfg4_nn)
-            a, p = upload(*host, dev)
-            desc = f"cfg4: block transport {args.cfg4_nn}^3 nodes x 10, smoothed aggregation"
+            # generated on the device (csrc/ptap_gen.cu); the oracle gets a host copy
+            a, p = devgen.block_transport_dist(args.cfg4_nn, 1, 0, dev)
+            desc = f"cfg4: block transport {args.cfg4_nn}^3 nodes x 10, smoothed aggregation (device-generated)"
+            if name in want_oracle:
+                host = host_copy(a, p)
         elif name == "cfg5":
-            from paper_1905_08423_b200 import problems_amg as amg
-            host = amg.knn_laplacian(args.cfg5_npts)
-            a, p = upload(*host, dev)
-            desc = f"cfg5: 26-NN Laplacian, {args.cfg5_npts} points, greedy aggregation"
+            a, p = devgen.knn_laplacian_dist(args.cfg5_npts, 1, 0, dev)
+            torch.cuda.empty_cache()
+            desc = f"cfg5: 26-NN Laplacian, {args.cfg5_npts} points, greedy aggregation (device-generated)"
+            if name in want_oracle:
+                host = host_copy(a, p)
         else:
             raise SystemExit(f"unknown config {name}")
         gen_s = time.perf_counter() - t
