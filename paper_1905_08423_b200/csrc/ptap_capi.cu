@@ -1186,8 +1186,11 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   p->cnt.kernel_launches += 2;
   l.nloc = (int32_t)n;
   l.ntiles = ntiles;
-  l.acap = (int32_t)((h[5] + 4 + 3) & ~3ull);
+  l.ast = (int32_t)(std::max<unsigned long long>(1, h[6]) | 1);
+  // the staged column region also holds the transposed converted rows (2 groups x 32 rows x ast)
+  l.acap = (int32_t)((std::max<unsigned long long>(h[5] + 4, (unsigned long long)LOCK_TILE * l.ast) + 3) & ~3ull);
   l.aps = (int32_t)(std::max<int64_t>(1, p->max_nap) | 1);
+  l.dbg = getenv("PTAP_LOCK_DBG") ? atoi(getenv("PTAP_LOCK_DBG")) : 0;
   if (h[4] != 0 || lock_smem_bytes(l) > 200 * 1024 || h[1] >= (1ull << 31) || h[2] >= (1ull << 31)) {
     if (getenv("PTAP_TRACE"))
       fprintf(stderr, "[ptap] lockstep plan: not eligible (%llu flagged, tile of %llu entries)\n", h[4], h[5]);

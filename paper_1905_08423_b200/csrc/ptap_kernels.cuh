@@ -264,6 +264,8 @@ struct __align__(16) LockClass {  // one structural class of fine rows (32 bytes
 struct LockArgs {
   int32_t nloc, ntiles, acap, aps;  // acap: staged A entries per tile, aps: AP buffer stride (doubles, odd)
   uint32_t fold_zero;               // index of eight zero entries behind the fold programs
+  int32_t ast;                      // odd stride (words) of the converted column rows, >= the longest A row
+  int32_t dbg;                      // timing experiments only (PTAP_LOCK_DBG): 1 no outer products, 2 no fold, 4 no column conversion
   const uint32_t *pq;       // [nloc] Q index of the first entry of P row k
   double *Q;                // [nnz(P_d)] P's values, class-major (rewritten every pass)
   const int32_t *cbQ;       // [nnz(P_d)] C row start of every P entry, same order

@@ -170,13 +170,29 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
   const uint32_t aval_sa = sm_u32(aval), acol_sa = sm_u32(acol);
   const uint32_t ap_sa0 = sm_u32(ap), tgv_sa = sm_u32(tgv), tgc_sa = sm_u32(tgc);
 
-  // columns -> Q index of the column's P row (in place), the row's own P entries
-  if (sub_all > 0) {
-#pragma unroll 4
-    for (int j = w; j < K_alen; j += LW) {
-      const uint32_t c = acol[rsl + j];
-      acol[rsl + j] = __ldg(la.pq + c);
-    }
+  // columns -> Q index of the column's P row.  The raw tile keeps rows of one
+  // parity an even number of words apart (2-way bank conflicts for a lane per
+  // row), so the converted indices are written back transposed: sorted row r
+  // of group g at the odd stride la.ast, conflict-free for the fold.  All raw
+  // columns are read (into registers) before any converted one is written.
+  constexpr int CQ = 32 / LW;
+  uint32_t cq[CQ];
+  const bool conv = sub_all > 0 && !(la.dbg & 4);
+#pragma unroll
+  for (int jj = 0; jj < CQ; ++jj) {
+    const int j = w + jj * LW;
+    cq[jj] = 0u;
+    if (conv && j < K_alen) cq[jj] = __ldg(la.pq + acol[rsl + j]);
+  }
+  __syncthreads();
+  const uint32_t c_row_sa = acol_sa + (uint32_t)((g * 32 + lane) * la.ast) * 4u;
+#pragma unroll
+  for (int jj = 0; jj < CQ; ++jj) {
+    const int j = w + jj * LW;
+    if (conv && j < K_alen)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(c_row_sa + (uint32_t)j * 4u), "r"(cq[jj]) : "memory");
+  }
+  if (conv) {
     const uint32_t pqi = __ldg(la.pq + i);
     for (int jt = w; jt < K_ntg; jt += LW) {
       const size_t x = (size_t)pqi + (size_t)jt * K_tstride;
@@ -196,7 +212,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     const int nchmax = __reduce_max_sync(FULLM, nch);
     const uint2 *fp = la.fold + K_fold_off + (size_t)sub_lo * 8;
     const uint32_t a_sa = sub_all > 0 ? aval_sa + (uint32_t)rsl * 8u : aval_sa;
-    const uint32_t c_sa = sub_all > 0 ? acol_sa + (uint32_t)rsl * 4u : sm_u32(rs + LT + 2);
+    const uint32_t c_sa = sub_all > 0 ? c_row_sa : sm_u32(rs + LT + 2);
     uint32_t o_sa = ap_sa0 + (uint32_t)(lane * la.aps + slot0) * 8u;
     double acc = 0.0;
     const uint2 *zchunk = la.fold + la.fold_zero;  // eight zero entries
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     uint2 ea[8], eb[8];
     load(ea, 0);
 #pragma unroll 1
-    for (int c = 0; c < nchmax; c += 2) {
+    for (int c = 0; c < ((la.dbg & 2) ? 0 : nchmax); c += 2) {
       load(eb, c + 1);
       process(ea);
       if (c + 1 < nchmax) {
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     uint32_t cached = 0xffffffffu;
     uint32_t s0a = 0, tv0 = 0, tc0 = 0, ps0 = 0, s1a = 0, tv1 = 0, tc1 = 0, ps1 = 0;
     bool ok0 = false, ok1 = false;
-    for (int r = w; r < cnt; r += LW) {
+    for (int r = w; r < ((la.dbg & 1) ? 0 : cnt); r += LW) {
       const uint32_t off = __shfl_sync(FULLM, K_outer_off, r);
       const int nit = __shfl_sync(FULLM, K_niter, r);
       if (off != cached) {
@@ -690,6 +706,10 @@ __global__ void __launch_bounds__(LOCK_TILE) k_lock_rowinfo(int64_t n, const int
   for (int k = 0; k < LT; ++k) rank += key[k] < mine;
   if (q < nr) rowinfo[r0 + rank] = ((uint32_t)(mine >> 6) << 8) | (uint32_t)q;
   if (q == 0) atomicMax(amax, (unsigned long long)(ad_rp[r0 + nr] - ad_rp[r0]));
+  // the longest A row -> amax[1]
+  const int alen = q < nr ? (int)(ad_rp[r0 + q + 1] - ad_rp[r0 + q]) : 0;
+  const int wmax = __reduce_max_sync(FULLM, alen);
+  if ((q & 31) == 0) atomicMax(amax + 1, (unsigned long long)wmax);
 }
 
 cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64_t *smap_rp, const int64_t *pmap_rp,
