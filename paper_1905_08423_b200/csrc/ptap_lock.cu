@@ -268,35 +268,23 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     uint32_t cached = 0xffffffffu;
     uint32_t s0a = 0, tv0 = 0, tc0 = 0, ps0 = 0, s1a = 0, tv1 = 0, tc1 = 0, ps1 = 0;
     bool ok0 = false, ok1 = false;
-    for (int r = w; r < ((la.dbg & 1) ? 0 : cnt); r += LW) {
-      const uint32_t off = __shfl_sync(FULLM, K_outer_off, r);
-      const int nit = __shfl_sync(FULLM, K_niter, r);
-      if (off != cached) {
-        const uint32_t wd0 = nit > 0 ? __ldg(la.outer + off + lane) : 0xffffffffu;
-        const uint32_t wd1 = nit > 1 ? __ldg(la.outer + off + 32 + lane) : 0xffffffffu;
-        ok0 = wd0 != 0xffffffffu;
-        ok1 = wd1 != 0xffffffffu;
-        s0a = ap_sa0 + (wd0 & 0xffu);
-        tv0 = tgv_sa + ((wd0 >> 8) & 0xffu) * (TGS * 8u);
-        tc0 = tgc_sa + ((wd0 >> 8) & 0xffu) * (TGS * 4u);
-        ps0 = wd0 >> 16;
-        s1a = ap_sa0 + (wd1 & 0xffu);
-        tv1 = tgv_sa + ((wd1 >> 8) & 0xffu) * (TGS * 8u);
-        tc1 = tgc_sa + ((wd1 >> 8) & 0xffu) * (TGS * 4u);
-        ps1 = wd1 >> 16;
-        cached = off;
-      }
+    auto decode = [&](uint32_t off, int nit) {
+      const uint32_t wd0 = nit > 0 ? __ldg(la.outer + off + lane) : 0xffffffffu;
+      const uint32_t wd1 = nit > 1 ? __ldg(la.outer + off + 32 + lane) : 0xffffffffu;
+      ok0 = wd0 != 0xffffffffu;
+      ok1 = wd1 != 0xffffffffu;
+      s0a = ap_sa0 + (wd0 & 0xffu);
+      tv0 = tgv_sa + ((wd0 >> 8) & 0xffu) * (TGS * 8u);
+      tc0 = tgc_sa + ((wd0 >> 8) & 0xffu) * (TGS * 4u);
+      ps0 = wd0 >> 16;
+      s1a = ap_sa0 + (wd1 & 0xffu);
+      tv1 = tgv_sa + ((wd1 >> 8) & 0xffu) * (TGS * 8u);
+      tc1 = tgc_sa + ((wd1 >> 8) & 0xffu) * (TGS * 4u);
+      ps1 = wd1 >> 16;
+      cached = off;
+    };
+    auto tail = [&](uint32_t off, int nit, int r) {  // rounds past the two cached ones (classes with > 64 items)
       const uint32_t ro = (uint32_t)r * rstride, r8 = (uint32_t)r * 8u, r4 = (uint32_t)r * 4u;
-      if (ok0) {
-        const double apv = lk_lds_f64(s0a + ro), tv = lk_lds_f64(tv0 + r8);
-        const uint32_t cb = lk_lds_u32(tc0 + r4);
-        atomicAdd(c_val + (cb + ps0), tv * apv);
-      }
-      if (ok1) {
-        const double apv = lk_lds_f64(s1a + ro), tv = lk_lds_f64(tv1 + r8);
-        const uint32_t cb = lk_lds_u32(tc1 + r4);
-        atomicAdd(c_val + (cb + ps1), tv * apv);
-      }
       for (int u = 2; u < nit; ++u) {
         const uint32_t wd = __ldg(la.outer + off + u * 32 + lane);
         if (wd != 0xffffffffu) {
@@ -306,6 +294,48 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
           const uint32_t cb = lk_lds_u32(tgc_sa + jt * (TGS * 4u) + r4);
           atomicAdd(c_val + (cb + (wd >> 16)), tv * apv);
         }
+      }
+    };
+    // two rows per step (all their operands loaded before the reductions)
+    // while both are of the cached class; otherwise one row at a time
+    for (int r = w; r < ((la.dbg & 1) ? 0 : cnt); r += 2 * LW) {
+      const int rb = r + LW;
+      const bool hasb = rb < cnt;
+      const uint32_t off = __shfl_sync(FULLM, K_outer_off, r);
+      const int nit = __shfl_sync(FULLM, K_niter, r);
+      const uint32_t offb = __shfl_sync(FULLM, K_outer_off, hasb ? rb : r);
+      const int nitb = __shfl_sync(FULLM, K_niter, hasb ? rb : r);
+      if (off != cached) decode(off, nit);
+      const bool pair = hasb && offb == off;
+      const uint32_t ro = (uint32_t)r * rstride, r8 = (uint32_t)r * 8u, r4 = (uint32_t)r * 4u;
+      const uint32_t rob = (uint32_t)rb * rstride, rb8 = (uint32_t)rb * 8u, rb4 = (uint32_t)rb * 4u;
+      double apv[4], tv[4];
+      uint32_t cb[4];
+      const bool on[4] = {ok0, ok1, ok0 && pair, ok1 && pair};
+      if (on[0]) { apv[0] = lk_lds_f64(s0a + ro); tv[0] = lk_lds_f64(tv0 + r8); cb[0] = lk_lds_u32(tc0 + r4); }
+      if (on[1]) { apv[1] = lk_lds_f64(s1a + ro); tv[1] = lk_lds_f64(tv1 + r8); cb[1] = lk_lds_u32(tc1 + r4); }
+      if (on[2]) { apv[2] = lk_lds_f64(s0a + rob); tv[2] = lk_lds_f64(tv0 + rb8); cb[2] = lk_lds_u32(tc0 + rb4); }
+      if (on[3]) { apv[3] = lk_lds_f64(s1a + rob); tv[3] = lk_lds_f64(tv1 + rb8); cb[3] = lk_lds_u32(tc1 + rb4); }
+      if (on[0]) atomicAdd(c_val + (cb[0] + ps0), tv[0] * apv[0]);
+      if (on[1]) atomicAdd(c_val + (cb[1] + ps1), tv[1] * apv[1]);
+      if (on[2]) atomicAdd(c_val + (cb[2] + ps0), tv[2] * apv[2]);
+      if (on[3]) atomicAdd(c_val + (cb[3] + ps1), tv[3] * apv[3]);
+      if (nit > 2) tail(off, nit, r);
+      if (pair) {
+        if (nitb > 2) tail(offb, nitb, rb);
+      } else if (hasb) {  // the second row is of another class
+        decode(offb, nitb);
+        if (ok0) {
+          const double a = lk_lds_f64(s0a + rob), t = lk_lds_f64(tv0 + rb8);
+          const uint32_t c = lk_lds_u32(tc0 + rb4);
+          atomicAdd(c_val + (c + ps0), t * a);
+        }
+        if (ok1) {
+          const double a = lk_lds_f64(s1a + rob), t = lk_lds_f64(tv1 + rb8);
+          const uint32_t c = lk_lds_u32(tc1 + rb4);
+          atomicAdd(c_val + (c + ps1), t * a);
+        }
+        if (nitb > 2) tail(offb, nitb, rb);
       }
     }
   }
