@@ -1123,10 +1123,14 @@ void free_lock(ptap_plan *p, cudaStream_t st) {
 // Eligible: the q4a plan (one-rank structure, A rows <= 32 entries) with
 // interned maps, AP rows <= 32 slots, P rows <= 8 entries, fewer than 32768
 // row classes, the C-row-start map, and a tile that fits shared memory.
-ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st) {
+// `pure` (several ranks): device flags of the rows without A_o / P_o parts (own
+// or neighbours'); only tiles inside runs of such rows are launched
+// (build_q4a_runs), the other rows share one empty class.
+ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cudaStream_t st,
+                       const uint8_t *pure = nullptr) {
   p->lock = false;
   if (getenv("PTAP_NO_LOCK") || p->lock_opt == 0) return PTAP_OK;
-  if (!p->mapped || !p->q4a || p->tile || p->alg == PTAP_TWO_STEP || p->max_nap > 32 || !p->maps.cbase)
+  if (!p->mapped || !(p->q4a || pure) || p->tile || p->alg == PTAP_TWO_STEP || p->max_nap > 32 || !p->maps.cbase)
     return PTAP_OK;
   const int64_t n = p->nloc, pnnz = ops->p_diag.nnz;
   if (n <= 0 || p->ncl <= 0 || pnnz <= 0 || pnnz >= INT32_MAX || ops->a_diag.nnz >= INT32_MAX ||
@@ -1161,7 +1165,7 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   CKS(palloc(p, &slot2cls, LOCK_TABLE, CAT_TRANSIENT, st));
   CKS(palloc(p, &slot_of, n, CAT_TRANSIENT, st));
   CK(launch_lock_classes(op, plen8, p->maps.smap_rp, p->maps.pmap_rp, keys, rep, LOCK_TABLE, slot_of, slot2cls, reps,
-                         st8, st8 + 4, st));
+                         st8, st8 + 4, pure, st));
   unsigned long long h[8];
   CK(cudaMemcpyAsync(h, st8, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1177,7 +1181,7 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   LockClass *cls = nullptr;
   CKS(palloc(p, &cls, ncls, CAT_PLAN, st));
   l.cls = cls;
-  CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, st));
+  CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, pure, st));
   CKS(palloc(p, &rowinfo, n, CAT_PLAN, st));
   l.rowinfo = rowinfo;
   CK(launch_lock_rowinfo(n, op.ad_rp, slot_of, slot2cls, rowinfo, st8 + 5, st));
@@ -1213,7 +1217,7 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   CKS(palloc(p, &cbq, pnnz, CAT_PLAN, st));
   CK(launch_lock_permute_i32(n, op.pd_rp, pq, ltab, p->maps.cbase, cbq, st));
   l.cbQ = cbq;
-  pfree(p, p->maps.cbase, st);
+  if (!pure) pfree(p, p->maps.cbase, st);  // several ranks: the runs' unaligned edges keep the per-row kernel
   CKS(palloc(p, &Q, pnnz, CAT_PLAN, st));
   l.Q = Q;
   p->cnt.kernel_launches += 3;
@@ -1593,8 +1597,11 @@ ptap_status build_q4a_runs(ptap_plan *p, const Ops &op, const ptap_operands *ops
   if (b0) CK(cudaMemcpyAsync(rows.data(), b0, nb0 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   else for (int64_t i = 0; i < nb0; ++i) rows[i] = (int32_t)i;
   CK(cudaStreamSynchronize(st));
-  pfree(p, flag, st);
   p->cnt.kernel_launches++;
+  struct FlagGuard {
+    ptap_plan *p; uint8_t *&f; cudaStream_t st;
+    ~FlagGuard() { pfree(p, f, st); }
+  } guard{p, flag, st};
   std::vector<std::pair<int64_t, int64_t>> runs;
   for (int64_t i = 0; i < n;) {
     if (!hf[i]) { ++i; continue; }
@@ -1622,6 +1629,9 @@ ptap_status build_q4a_runs(ptap_plan *p, const Ops &op, const ptap_operands *ops
     p->cnt.kernel_launches++;
   }
   p->qa_runs = runs;
+  // the runs' whole 64-row tiles take the class-lockstep pass
+  CKS(build_lock(p, op, ops, st, flag));
+  if (p->lock) p->cnt.numeric_path = 3;
   if (getenv("PTAP_TRACE")) {
     int64_t in = 0;
     for (auto &r : runs) in += r.second;
@@ -1638,9 +1648,30 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
       if (bs.count[q] == 0) continue;
       const int32_t *rows = (q == 0 && bs.identity0) ? nullptr : bs.rows[q];
       if (q == 0 && !p->qa_runs.empty() && &bs == &p->bins_local && do_local && !do_send) {
-        for (auto &r : p->qa_runs) {
-          CK(launch_outer_numeric_q4a(op, (unsigned long long)r.second, p->maps, tg, p->d_status, st, (int)r.first));
+        const bool lk = lock_usable(p, op);
+        if (lk) {
+          CK(launch_lock_permute_f64(p->nloc, op.pd_rp, p->la.pq, p->la.ltab, op.pd_val, p->la.Q, st));
           p->cnt.kernel_launches++;
+        }
+        for (auto &r : p->qa_runs) {
+          int64_t lo = r.first, hi = r.first + r.second;
+          if (lk) {  // whole tiles inside the run in lockstep, its edges row by row
+            const int64_t t0 = (lo + LOCK_TILE - 1) / LOCK_TILE, t1 = hi / LOCK_TILE;
+            if (t1 > t0) {
+              if (t0 * LOCK_TILE > lo) {
+                CK(launch_outer_numeric_q4a(op, (unsigned long long)(t0 * LOCK_TILE - lo), p->maps, tg, p->d_status, st,
+                                            (int)lo));
+                p->cnt.kernel_launches++;
+              }
+              CK(launch_lock_numeric(op, p->la, p->c_val, (int)t0, (int)t1, st));
+              p->cnt.kernel_launches++;
+              lo = t1 * LOCK_TILE;
+            }
+          }
+          if (hi > lo) {
+            CK(launch_outer_numeric_q4a(op, (unsigned long long)(hi - lo), p->maps, tg, p->d_status, st, (int)lo));
+            p->cnt.kernel_launches++;
+          }
         }
         if (p->qa_rest_n > 0) {
           CK(launch_outer_numeric_mapped(3, op, p->qa_rest, (unsigned long long)p->qa_rest_n, p->maps, tg, do_send,
@@ -2118,7 +2149,7 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
   }
   if ((flags & 1) && p->c_nnz > 0) CK(cudaMemsetAsync(p->c_val, 0, sizeof(double) * p->c_nnz, st));
   OuterTargets tg{p->c_rp, p->c_col, p->c_val, p->s_nrows, p->s_rows, p->s_rp, p->s_col, p->s_val};
-  if (lock_usable(p, op) && row_lo % LOCK_TILE == 0 && (row_hi % LOCK_TILE == 0 || row_hi == p->nloc)) {
+  if (p->q4a && lock_usable(p, op) && row_lo % LOCK_TILE == 0 && (row_hi % LOCK_TILE == 0 || row_hi == p->nloc)) {
     if (flags & 1) {
       CK(launch_lock_permute_f64(p->nloc, op.pd_rp, p->la.pq, p->la.ltab, op.pd_val, p->la.Q, st));
       p->cnt.kernel_launches++;

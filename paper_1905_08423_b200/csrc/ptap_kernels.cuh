@@ -287,10 +287,11 @@ cudaError_t launch_lock_permute_i32(int64_t n, const int64_t *pd_rp, const uint3
 cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64_t *smap_rp, const int64_t *pmap_rp,
                                 unsigned long long *keys, uint32_t *rep, int tbl, uint16_t *slot_of,
                                 int32_t *slot2cls, uint32_t *reps, unsigned long long *out, unsigned long long *bad,
-                                cudaStream_t st);
+                                const uint8_t *pure, cudaStream_t st);
 cudaError_t launch_lock_headers(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                 const uint32_t *reps, const int32_t *ltab, LockClass *cls,
-                                unsigned long long *out, unsigned long long *bad, cudaStream_t st);
+                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure,
+                                cudaStream_t st);
 cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                  const uint32_t *reps, const int32_t *ltab, const LockClass *cls, uint2 *fold,
                                  uint32_t *outer, cudaStream_t st);

@@ -503,13 +503,14 @@ __device__ __forceinline__ unsigned long long lock_row_key(const Ops &op, const 
 __global__ void __launch_bounds__(256) k_lock_claim(Ops op, const uint8_t *plen8, const int64_t *smap_rp,
                                                     const int64_t *pmap_rp, unsigned long long *keys, uint32_t *rep,
                                                     uint32_t mask, uint16_t *slot_of, unsigned long long *nclaim,
-                                                    unsigned long long *bad) {
+                                                    unsigned long long *bad, const uint8_t *pure) {
   const int gl = threadIdx.x & (CG - 1);
   const int64_t i = ((int64_t)blockIdx.x * 256 + threadIdx.x) / CG;
   const bool in = i < op.nloc;
   int alen = 0;
-  const unsigned long long h = lock_row_key(op, plen8, smap_rp, pmap_rp, in ? i : 0, gl, alen);
+  unsigned long long h = lock_row_key(op, plen8, smap_rp, pmap_rp, in ? i : 0, gl, alen);
   if (!in || gl) return;
+  if (pure && !pure[i]) h = 2ull;  // rows with A_o / P_o parts (several ranks) never run here: one empty class
   uint32_t s = (uint32_t)(h >> 17) & mask;
   for (int probe = 0; probe < 128; ++probe, s = (s + 1) & mask) {
     unsigned long long cur = *(volatile unsigned long long *)(keys + s);
@@ -532,10 +533,11 @@ __global__ void __launch_bounds__(256) k_lock_claim(Ops op, const uint8_t *plen8
 
 __global__ void __launch_bounds__(256) k_lock_verify(Ops op, const uint8_t *plen8, const int64_t *smap_rp,
                                                      const int64_t *pmap_rp, const uint32_t *rep,
-                                                     const uint16_t *slot_of, unsigned long long *bad) {
+                                                     const uint16_t *slot_of, unsigned long long *bad,
+                                                     const uint8_t *pure) {
   const int gl = threadIdx.x & (CG - 1);
   const int64_t i = ((int64_t)blockIdx.x * 256 + threadIdx.x) / CG;
-  if (i >= op.nloc) return;
+  if (i >= op.nloc || (pure && !pure[i])) return;
   const int64_t r = rep[slot_of[i]];
   if (r == i) return;
   bool ok = r < op.nloc;
@@ -604,7 +606,7 @@ __device__ void lock_class_split(const Ops &op, const uint8_t *plen8, const uint
 __global__ void __launch_bounds__(1024) k_lock_headers(int ncls, Ops op, const uint8_t *plen8, const int64_t *smap_rp,
                                                        const uint8_t *smap, const uint8_t *nap, const uint32_t *reps,
                                                        const int32_t *ltab, LockClass *cls, unsigned long long *out,
-                                                       unsigned long long *bad) {
+                                                       unsigned long long *bad, const uint8_t *pure) {
   typedef cub::BlockScan<unsigned, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned carry_f, carry_o;
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(1024) k_lock_headers(int ncls, Ops op, const u
     const int c = base + threadIdx.x;
     LockClass K{};
     unsigned fsz = 0, osz = 0;
-    if (c < ncls) {
+    if (c < ncls && !(pure && !pure[reps[c]])) {
       const int64_t r = reps[c];
       const int64_t a0 = __ldg(op.ad_rp + r);
       const int alen = (int)(__ldg(op.ad_rp + r + 1) - a0), napr = nap[r], ntg = plen8[r];
@@ -745,23 +747,25 @@ __global__ void __launch_bounds__(LOCK_TILE) k_lock_rowinfo(int64_t n, const int
 cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64_t *smap_rp, const int64_t *pmap_rp,
                                 unsigned long long *keys, uint32_t *rep, int tbl, uint16_t *slot_of,
                                 int32_t *slot2cls, uint32_t *reps, unsigned long long *out, unsigned long long *bad,
-                                cudaStream_t st) {
+                                const uint8_t *pure, cudaStream_t st) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * tbl, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(rep, 0xff, sizeof(uint32_t) * tbl, st)) != cudaSuccess) return e;
   const int64_t threads = op.nloc * CG;
   const int nb = (int)((threads + 255) / 256);
   if (nb == 0) return cudaSuccess;
-  k_lock_claim<<<nb, 256, 0, st>>>(op, plen8, smap_rp, pmap_rp, keys, rep, (uint32_t)(tbl - 1), slot_of, out + 3, bad);
-  k_lock_verify<<<nb, 256, 0, st>>>(op, plen8, smap_rp, pmap_rp, rep, slot_of, bad);
+  k_lock_claim<<<nb, 256, 0, st>>>(op, plen8, smap_rp, pmap_rp, keys, rep, (uint32_t)(tbl - 1), slot_of, out + 3, bad,
+                                   pure);
+  k_lock_verify<<<nb, 256, 0, st>>>(op, plen8, smap_rp, pmap_rp, rep, slot_of, bad, pure);
   k_lock_compact<<<1, 1024, 0, st>>>(tbl, keys, rep, slot2cls, reps, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lock_headers(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                 const uint32_t *reps, const int32_t *ltab, LockClass *cls,
-                                unsigned long long *out, unsigned long long *bad, cudaStream_t st) {
-  k_lock_headers<<<1, 1024, 0, st>>>(ncls, op, plen8, mp.smap_rp, mp.smap, mp.nap, reps, ltab, cls, out, bad);
+                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure,
+                                cudaStream_t st) {
+  k_lock_headers<<<1, 1024, 0, st>>>(ncls, op, plen8, mp.smap_rp, mp.smap, mp.nap, reps, ltab, cls, out, bad, pure);
   return cudaGetLastError();
 }
 

@@ -122,3 +122,41 @@ def test_single_shot_falls_back_when_rows_are_exchanged():
     g = pk.assemble_global([r[0] for r in res], ncols=P.ncols)
     assert np.array_equal(g.row_offsets, want.row_ptr) and np.array_equal(g.col_indices, want.col)
     assert row_scaled_err(want.row_ptr, g.values, want.val) <= TOL
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+def test_lockstep_runs_inside_rank_interiors(nr):
+    """Several ranks (gloo, one GPU): the rows of a z-slab without off-rank
+    parts form long runs; their whole 64-row tiles take the lockstep kernel
+    (numeric_path 3), the slab faces and the runs' edges the per-row kernels.
+    C matches the oracle at the same rank count; a second pass after scaling
+    A scales C."""
+    from oracle.oracle import oracle_ptap
+
+    A, P = gen.config_operands(gen.CONFIGS["cfg3"], n_fine=24)
+    want = oracle_ptap(A.nrows, P.ncols, A.row_offsets, A.col_indices, A.values, P.row_offsets, P.col_indices,
+                       P.values, nranks=nr, algorithm="allatonce")
+
+    def prog(ctx):
+        import copy
+
+        a, p = pk.distribute(A, P, ctx.nranks, ctx.rank)
+        plan = pk.run_symbolic(a, p, "allatonce", ctx)
+        pk.run_numeric(a, p, plan, ctx)
+        path = plan.device_counters()["numeric_path"]
+        a.local.diag.values *= 2.0
+        a.local.offdiag.values *= 2.0
+        c2 = copy.deepcopy(pk.run_numeric(a, p, plan, ctx))
+        a.local.diag.values /= 2.0
+        a.local.offdiag.values /= 2.0
+        c3 = pk.run_numeric(a, p, plan, ctx)
+        return c3, path, c2
+
+    res = pk.spawn_ranks(nr, prog)
+    assert all(r[1] == 3 for r in res), [r[1] for r in res]
+    g = pk.assemble_global([r[0] for r in res], ncols=P.ncols)
+    pattern = np.array_equal(g.row_offsets, want.row_ptr) and np.array_equal(g.col_indices, want.col)
+    assert pattern
+    assert row_scaled_err(want.row_ptr, g.values, want.val) <= TOL
+    g2 = pk.assemble_global([r[2] for r in res], ncols=P.ncols)
+    assert row_scaled_err(want.row_ptr, g2.values, 2.0 * want.val) <= TOL
