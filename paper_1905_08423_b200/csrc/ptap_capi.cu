@@ -1663,7 +1663,7 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
                                             (int)lo));
                 p->cnt.kernel_launches++;
               }
-              CK(launch_lock_numeric(op, p->la, p->c_val, (int)t0, (int)t1, st));
+              CK(launch_lock_numeric(op, p->la, p->c_val, (int)t0, (int)t1, p->d_status, st));
               p->cnt.kernel_launches++;
               lo = t1 * LOCK_TILE;
             }
@@ -1690,7 +1690,7 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
         }
         if (lock_usable(p, op)) {  // rows of one class in lockstep; P's values class-major first
           CK(launch_lock_permute_f64(p->nloc, op.pd_rp, p->la.pq, p->la.ltab, op.pd_val, p->la.Q, st));
-          CK(launch_lock_numeric(op, p->la, p->c_val, 0, p->la.ntiles, st));
+          CK(launch_lock_numeric(op, p->la, p->c_val, 0, p->la.ntiles, p->d_status, st));
           p->cnt.kernel_launches += 2;
           continue;
         }
@@ -2155,7 +2155,7 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
       p->cnt.kernel_launches++;
     }
     CK(launch_lock_numeric(op, p->la, p->c_val, (int)(row_lo / LOCK_TILE),
-                           (int)((row_hi + LOCK_TILE - 1) / LOCK_TILE), st));
+                           (int)((row_hi + LOCK_TILE - 1) / LOCK_TILE), p->d_status, st));
     p->cnt.kernel_launches++;
     p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
   } else if (row_hi > row_lo) {

@@ -277,7 +277,7 @@ struct LockArgs {
 };
 size_t lock_smem_bytes(const LockArgs &la);
 cudaError_t launch_lock_numeric(const Ops &op, const LockArgs &la, double *c_val, int tile_lo, int tile_hi,
-                                cudaStream_t st);
+                                int *status, cudaStream_t st);
 cudaError_t launch_lock_qlayout(int64_t n, const int64_t *pd_rp, uint8_t *plen8, int32_t *blkcnt, int32_t *ltab,
                                 uint32_t *pq, unsigned long long *bad, cudaStream_t st);
 cudaError_t launch_lock_permute_f64(int64_t n, const int64_t *pd_rp, const uint32_t *pq, const int32_t *ltab,

@@ -111,7 +111,7 @@ __device__ __forceinline__ void lk_group_bar(int g) {
 }
 
 __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs la, double *__restrict__ c_val,
-                                                               int tile0) {
+                                                               int tile0, int *status) {
   extern __shared__ __align__(16) unsigned char lsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / LW, w = warp - g * LW;
@@ -129,6 +129,10 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
   const int r0 = tile * LT, r1 = min(r0 + LT, la.nloc);
   const int64_t a0 = __ldg(op.ad_rp + r0), a1 = __ldg(op.ad_rp + r1);
   const int64_t c0 = a0 & ~3ll, cend = a1 & ~3ll;
+  if (a1 < a0 || a1 - c0 > (int64_t)la.acap) {  // A's row offsets are not the symbolic ones
+    if (tid == 0) atomicOr(status, ST_DRIFT);
+    return;
+  }
   if (tid == 0) lk_mbar_init(bar, 1);
   __syncthreads();
   if (tid == 0) {
@@ -158,15 +162,19 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
     k0 = __ldg(kp);
     k1 = __ldg(kp + 1);
   }
+  __syncthreads();
+  lk_mbar_wait(bar, 0);
+  if (cnt <= 0) return;
+  const int i = r0 + q, rsl = rs[q];
+  if (active && rs[q + 1] - rsl != (int)(k0.x & 0xffu)) {  // not the row its class was built from
+    atomicOr(status, ST_DRIFT);
+    k0 = k1 = make_uint4(0u, 0u, 0u, 0u);
+  }
   const int K_alen = (int)(k0.x & 0xffu), K_ntg = (int)((k0.x >> 16) & 0xffu), K_niter = (int)(k0.x >> 24);
   const uint32_t K_tstride = k0.y, K_fold_off = k0.z, K_outer_off = k0.w;
   const unsigned long long K_sub = ((unsigned long long)k1.y << 32) | k1.x, K_s0 = ((unsigned long long)k1.w << 32) | k1.z;
   const int sub_lo = (int)((K_sub >> (8 * w)) & 0xffu), sub_hi = (int)((K_sub >> (8 * (w + 1))) & 0xffu);
   const int sub_all = (int)((K_sub >> (8 * LW)) & 0xffu), slot0 = (int)((K_s0 >> (8 * w)) & 0xffu);
-  __syncthreads();
-  lk_mbar_wait(bar, 0);
-  if (cnt <= 0) return;
-  const int i = r0 + q, rsl = rs[q];
   const uint32_t aval_sa = sm_u32(aval), acol_sa = sm_u32(acol);
   const uint32_t ap_sa0 = sm_u32(ap), tgv_sa = sm_u32(tgv), tgc_sa = sm_u32(tgc);
 
@@ -347,7 +355,7 @@ size_t lock_smem_bytes(const LockArgs &la) {
 }
 
 cudaError_t launch_lock_numeric(const Ops &op, const LockArgs &la, double *c_val, int tile_lo, int tile_hi,
-                                cudaStream_t st) {
+                                int *status, cudaStream_t st) {
   if (tile_hi <= tile_lo) return cudaSuccess;
   const size_t sm = lock_smem_bytes(la);
   static size_t opted = 0;
@@ -356,7 +364,7 @@ cudaError_t launch_lock_numeric(const Ops &op, const LockArgs &la, double *c_val
     if (e != cudaSuccess) return e;
     opted = sm;
   }
-  k_lock_numeric<<<tile_hi - tile_lo, LG * LW * 32, sm, st>>>(op, la, c_val, tile_lo);
+  k_lock_numeric<<<tile_hi - tile_lo, LG * LW * 32, sm, st>>>(op, la, c_val, tile_lo, status);
   return cudaGetLastError();
 }
 

@@ -160,3 +160,26 @@ def test_lockstep_runs_inside_rank_interiors(nr):
     assert row_scaled_err(want.row_ptr, g.values, want.val) <= TOL
     g2 = pk.assemble_global([r[2] for r in res], ncols=P.ncols)
     assert row_scaled_err(want.row_ptr, g2.values, 2.0 * want.val) <= TOL
+
+
+def test_lockstep_kernel_flags_in_place_structure_edits():
+    """The lockstep kernel trusts the plan's classes; a row whose length no
+    longer matches its class (row offsets edited in place, sizes unchanged, so
+    the host-side size checks pass) is reported as structural drift instead of
+    reading past its staged row."""
+    from paper_1905_08423_b200 import devgen
+    from paper_1905_08423_b200.errors import StructuralDriftError
+
+    ctx = pk.single_rank_context()
+    a, p = devgen.config_dist("cfg3", 1, 0, ctx.device, n_fine=16)
+    plan = pk.run_symbolic(a, p, "allatonce", ctx)
+    assert plan.device_counters()["numeric_path"] == 3
+    pk.run_numeric_device(a, p, plan, ctx)
+    plan.check()
+    rp = a.local.diag.row_ptr
+    k = rp.numel() // 2
+    rp[k] += 1  # row k-1 one entry longer, row k one shorter
+    pk.run_numeric_device(a, p, plan, ctx)
+    with pytest.raises(StructuralDriftError):
+        plan.check()
+    rp[k] -= 1
