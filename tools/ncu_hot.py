@@ -1,14 +1,15 @@
 """Top SASS lines of an ncu report by stall samples, with the dominant stall
-reasons: python tools/ncu_hot.py report.ncu-rep [n]"""
+reasons: python tools/ncu_hot.py report.ncu-rep [n] [--kernel REGEX]"""
 import csv, io, subprocess, sys
 
 rep = sys.argv[1]
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout
+n = int(sys.argv[2]) if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else 25
+ksel = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
+out = subprocess.run(["ncu", "-i", rep, *ksel, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r != hdr]
 ix = {h: i for i, h in enumerate(hdr)}
 samp = ix["Warp Stall Sampling (All Samples)"]
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
