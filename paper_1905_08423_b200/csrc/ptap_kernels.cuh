@@ -251,7 +251,7 @@ constexpr int LOCK_TILE = 64;  // fine rows per tile
 constexpr int LOCK_NLEN = 9;   // P row lengths 0..8
 constexpr int LOCK_TABLE = 65536;  // class table slots (a plan with more than half as many classes is not eligible)
 #ifndef PTAP_LOCK_WARPS
-#define PTAP_LOCK_WARPS 2
+#define PTAP_LOCK_WARPS 3  // measured on config 3: 2 -> 4.91 ms, 3 -> 4.72, 4 -> 4.77
 #endif
 constexpr int LOCK_W = PTAP_LOCK_WARPS;  // warps per group of 32 rows (<= 7)
 struct __align__(16) LockClass {  // one structural class of fine rows (32 bytes)

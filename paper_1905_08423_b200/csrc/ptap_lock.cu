@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
   // row), so the converted indices are written back transposed: sorted row r
   // of group g at the odd stride la.ast, conflict-free for the fold.  All raw
   // columns are read (into registers) before any converted one is written.
-  constexpr int CQ = 32 / LW;
+  constexpr int CQ = (32 + LW - 1) / LW;
   uint32_t cq[CQ];
   const bool conv = sub_all > 0 && !(la.dbg & 4);
 #pragma unroll
