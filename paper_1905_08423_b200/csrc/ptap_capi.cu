@@ -1114,7 +1114,7 @@ ptap_status build_tile(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
 // ---- class-lockstep numeric plan (ptap_lock.cu) ------------------------------
 void free_lock(ptap_plan *p, cudaStream_t st) {
   LockArgs &l = p->la;
-  pfree(p, l.pq, st); pfree(p, l.Q, st); pfree(p, l.cbQ, st); pfree(p, l.rowinfo, st);
+  pfree(p, l.pq, st); pfree(p, l.Q, st); pfree(p, l.cbQ, st); pfree(p, l.rowinfo, st); pfree(p, l.rowcls, st);
   pfree(p, l.cls, st); pfree(p, l.fold, st); pfree(p, l.outer, st); pfree(p, l.ltab, st);
   l = LockArgs{};
   p->lock = false;
@@ -1130,7 +1130,9 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
                        const uint8_t *pure = nullptr) {
   p->lock = false;
   if (getenv("PTAP_NO_LOCK") || p->lock_opt == 0) return PTAP_OK;
-  if (!p->mapped || !(p->q4a || pure) || p->tile || p->alg == PTAP_TWO_STEP || p->max_nap > 32 || !p->maps.cbase)
+  const bool for_tile = p->tile;  // the deterministic kernel takes the classes, programs and Q for its fold
+  if (!p->mapped || !(p->q4a || pure) || p->alg == PTAP_TWO_STEP || p->max_nap > 32 ||
+      (!for_tile && !p->maps.cbase) || getenv("PTAP_TILE_NO_LOCKFOLD") && for_tile)
     return PTAP_OK;
   const int64_t n = p->nloc, pnnz = ops->p_diag.nnz;
   if (n <= 0 || p->ncl <= 0 || pnnz <= 0 || pnnz >= INT32_MAX || ops->a_diag.nnz >= INT32_MAX ||
@@ -1184,7 +1186,12 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, pure, st));
   CKS(palloc(p, &rowinfo, n, CAT_PLAN, st));
   l.rowinfo = rowinfo;
-  CK(launch_lock_rowinfo(n, op.ad_rp, slot_of, slot2cls, rowinfo, st8 + 5, st));
+  uint32_t *rowcls = nullptr;
+  if (for_tile) {
+    CKS(palloc(p, &rowcls, n, CAT_PLAN, st));
+    l.rowcls = rowcls;
+  }
+  CK(launch_lock_rowinfo(n, op.ad_rp, slot_of, slot2cls, rowinfo, rowcls, st8 + 5, st));
   CK(cudaMemcpyAsync(h, st8, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   p->cnt.kernel_launches += 2;
@@ -1214,10 +1221,12 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   // the C row starts in Q order replace the per-entry map of the q4a kernel
   int32_t *cbq = nullptr;
   double *Q = nullptr;
-  CKS(palloc(p, &cbq, pnnz, CAT_PLAN, st));
-  CK(launch_lock_permute_i32(n, op.pd_rp, pq, ltab, p->maps.cbase, cbq, st));
-  l.cbQ = cbq;
-  if (!pure) pfree(p, p->maps.cbase, st);  // several ranks: the runs' unaligned edges keep the per-row kernel
+  if (!for_tile) {
+    CKS(palloc(p, &cbq, pnnz, CAT_PLAN, st));
+    CK(launch_lock_permute_i32(n, op.pd_rp, pq, ltab, p->maps.cbase, cbq, st));
+    l.cbQ = cbq;
+    if (!pure) pfree(p, p->maps.cbase, st);  // several ranks: the runs' unaligned edges keep the per-row kernel
+  }
   CKS(palloc(p, &Q, pnnz, CAT_PLAN, st));
   l.Q = Q;
   p->cnt.kernel_launches += 3;
@@ -1265,7 +1274,10 @@ ptap_status build_maps(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
     p->cnt.numeric_path = 1;
     p->cnt.map_bytes = p->smap_bytes + p->pmap_bytes;
     CKS(build_tile(p, op, ops, st));
-    if (p->tile) p->cnt.numeric_path = 2;
+    if (p->tile) {
+      p->cnt.numeric_path = 2;
+      CKS(build_lock(p, op, ops, st));  // its fold walks the class programs when the plan is eligible
+    }
   }
   // C row start per P_d entry for the q4a outer phase (4 B per P entry)
   if (ok && p->q4a && !p->tile && p->c_nnz < INT32_MAX && !getenv("PTAP_NO_CBASE")) {
@@ -1684,7 +1696,8 @@ ptap_status run_outer_numeric(ptap_plan *p, const Ops &op, BinSet &bs, int do_se
       // half is empty and its fused loop is the local loop
       if (q == 0 && p->q4a && bs.identity0 && do_local && (!do_send || op.po_rp == nullptr)) {
         if (p->tile) {  // deterministic owner-computes pass: writes every C entry once
-          CK(launch_tile_numeric(op, p->maps, p->ta, p->c_rp, p->c_val, 0, p->ta.nblk, true, st));
+          CK(launch_tile_numeric(op, p->maps, p->ta, p->lock ? p->la : LockArgs{}, p->c_rp, p->c_val, 0, p->ta.nblk, true,
+                                 st));
           p->cnt.kernel_launches += 2;
           continue;
         }
@@ -2141,7 +2154,8 @@ ptap_status ptap_numeric_local_rows(ptap_plan *p, const ptap_operands *ops, int6
     if (row_lo % TILE_ROWS || (row_hi % TILE_ROWS && row_hi != p->nloc))
       return fail(PTAP_ERR_VALUE, "row range must be aligned to the plan's 64-row blocks");
     const int b0 = (int)(row_lo / TILE_ROWS), b1 = (int)((row_hi + TILE_ROWS - 1) / TILE_ROWS);
-    CK(launch_tile_numeric(op, p->maps, p->ta, p->c_rp, p->c_val, b0, b1, (flags & 1) != 0, st));
+    CK(launch_tile_numeric(op, p->maps, p->ta, p->lock ? p->la : LockArgs{}, p->c_rp, p->c_val, b0, b1,
+                           (flags & 1) != 0, st));
     p->cnt.kernel_launches += 2;
     p->cnt.numeric_row_kernel_calls += row_hi - row_lo;
     if (flags & 2) p->cnt.numeric_runs++;

@@ -223,8 +223,10 @@ cudaError_t launch_tile_pruns(int nblk, int64_t nloc, const int64_t *ad_rp, cons
                               const int64_t *pd_rp, int64_t pnnz, int pvcap, int prcap, uint8_t *pr_n, int2 *pr_k,
                               unsigned long long *stats, cudaStream_t st);
 size_t tile_scan_scratch(int64_t n);
-cudaError_t launch_tile_numeric(const Ops &op, const MapArgs &mp, const TileArgs &ta, const int64_t *c_rp,
-                                double *c_val, int blk_lo, int blk_hi, bool new_pass, cudaStream_t st);
+struct LockArgs;
+cudaError_t launch_tile_numeric(const Ops &op, const MapArgs &mp, const TileArgs &ta, const LockArgs &la,
+                                const int64_t *c_rp, double *c_val, int blk_lo, int blk_hi, bool new_pass,
+                                cudaStream_t st);
 cudaError_t launch_tile_transpose(int64_t n, int64_t ncl, const int64_t *pd_rp, const int32_t *pd_col,
                                   int64_t pnnz, int32_t *cnt, int32_t *t_rp, int32_t *cursor, int32_t *t_row,
                                   uint8_t *t_jx, void *scratch, size_t scratch_bytes, int *status,
@@ -270,6 +272,7 @@ struct LockArgs {
   double *Q;                // [nnz(P_d)] P's values, class-major (rewritten every pass)
   const int32_t *cbQ;       // [nnz(P_d)] C row start of every P entry, same order
   const uint32_t *rowinfo;  // [nloc] per tile, rows sorted by class: class << 8 | row - tile start
+  const uint32_t *rowcls;   // [nloc] class of every row (the deterministic kernel's lockstep fold)
   const LockClass *cls;
   const uint2 *fold;        // x: A entry*8 | last-of-slot << 15 | A entry*4 << 16, y: Q offset of the P entry
   const uint32_t *outer;    // slot*8 | target << 8 | position in the C row << 16
@@ -296,6 +299,6 @@ cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, 
                                  const uint32_t *reps, const int32_t *ltab, const LockClass *cls, uint2 *fold,
                                  uint32_t *outer, cudaStream_t st);
 cudaError_t launch_lock_rowinfo(int64_t n, const int64_t *ad_rp, const uint16_t *slot_of, const int32_t *slot2cls,
-                                uint32_t *rowinfo, unsigned long long *amax, cudaStream_t st);
+                                uint32_t *rowinfo, uint32_t *rowcls, unsigned long long *amax, cudaStream_t st);
 
 }  // namespace ptapdev

@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(128) k_lock_programs(int ncls, Ops op, const u
 // = class << 8 | row - tile start; the largest tile (A entries) -> amax
 __global__ void __launch_bounds__(LOCK_TILE) k_lock_rowinfo(int64_t n, const int64_t *ad_rp, const uint16_t *slot_of,
                                                             const int32_t *slot2cls, uint32_t *rowinfo,
-                                                            unsigned long long *amax) {
+                                                            uint32_t *rowcls, unsigned long long *amax) {
   __shared__ int key[LT];
   const int q = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * LT;
@@ -745,6 +745,7 @@ __global__ void __launch_bounds__(LOCK_TILE) k_lock_rowinfo(int64_t n, const int
   int rank = 0;
   for (int k = 0; k < LT; ++k) rank += key[k] < mine;
   if (q < nr) rowinfo[r0 + rank] = ((uint32_t)(mine >> 6) << 8) | (uint32_t)q;
+  if (q < nr && rowcls) rowcls[r0 + q] = (uint32_t)(mine >> 6);
   if (q == 0) atomicMax(amax, (unsigned long long)(ad_rp[r0 + nr] - ad_rp[r0]));
   // the longest A row -> amax[1]
   const int alen = q < nr ? (int)(ad_rp[r0 + q + 1] - ad_rp[r0 + q]) : 0;
@@ -787,10 +788,10 @@ cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, 
 }
 
 cudaError_t launch_lock_rowinfo(int64_t n, const int64_t *ad_rp, const uint16_t *slot_of, const int32_t *slot2cls,
-                                uint32_t *rowinfo, unsigned long long *amax, cudaStream_t st) {
+                                uint32_t *rowinfo, uint32_t *rowcls, unsigned long long *amax, cudaStream_t st) {
   const int nt = (int)((n + LT - 1) / LT);
   if (nt == 0) return cudaSuccess;
-  k_lock_rowinfo<<<nt, LT, 0, st>>>(n, ad_rp, slot_of, slot2cls, rowinfo, amax);
+  k_lock_rowinfo<<<nt, LT, 0, st>>>(n, ad_rp, slot_of, slot2cls, rowinfo, rowcls, amax);
   return cudaGetLastError();
 }
 

@@ -66,6 +66,7 @@ constexpr int MAXRUN = TILE_MAXRUN;
 struct TileTail {
   unsigned long long bar;
   int item, next, jb, nrun;
+  int zero;  // a zero word: lanes without a fold program read Q[0] through it
   int rk0[MAXRUN], rk1[MAXRUN], rvoff[MAXRUN], rpoff[MAXRUN];
 };
 
@@ -206,7 +207,7 @@ __device__ __forceinline__ void stage_block(const Ops &op, const TileArgs &ta, i
 // ---------------------------------------------------------------------------
 // the numeric kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric(Ops op, MapArgs mp, TileArgs ta, const int64_t *c_rp,
+__global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric(Ops op, MapArgs mp, TileArgs ta, LockArgs la, const int64_t *c_rp,
                                                           double *c_val, int blk_lo, int blk_hi, int item_hi) {
   extern __shared__ __align__(16) unsigned char tile_smem_raw[];
   double *aval = (double *)(tile_smem_raw + ta.sm_aval);
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric
   const int R = ta.ring_blocks;
   if (tid == 0) {
     mbar_init(&T.bar, 1);
+    T.zero = 0;
     T.item = blk_lo + (int)atomicAdd(ta.ctl, 1u);
   }
   __syncthreads();
@@ -254,6 +256,74 @@ __global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric
       bar_fold();
       // ---- fold: one row per lane, [slot][lane] accumulators ------------------
       double *acc = accall + warp * ta.napc * AST;
+      if (la.cls != nullptr && !(ta.dbg & 8)) {
+        // The class-lockstep fold (ptap_lock.cu): the lane walks its class's
+        // slot-major program -- per pair an A value and a Q row start from the
+        // staged block, a P value from the class-major copy Q -- with the
+        // reference's arithmetic: the first product of a slot sets it, the
+        // others are added in fold order, each multiply and add rounded on its
+        // own (src/_kernels.py:116-147), so AP rows keep the reference's bits.
+        uint4 k0 = make_uint4(0u, 0u, 0u, 0u), k1 = k0;
+        if (i < r1) {
+          const uint4 *kp = (const uint4 *)(la.cls + __ldg(la.rowcls + i));
+          k0 = __ldg(kp);
+          k1 = __ldg(kp + 1);
+        }
+        const int K_alen = (int)(k0.x & 0xffu);
+        const unsigned long long K_sub = ((unsigned long long)k1.y << 32) | k1.x;
+        const unsigned long long K_s0 = ((unsigned long long)k1.w << 32) | k1.z;
+        const bool prog = (int)((K_sub >> (8 * LOCK_W)) & 0xffu) > 0;
+        const int tc = (int)(arow - c0), tv = (int)(arow - v0);
+        if (prog)
+#pragma unroll 4
+          for (int j = 0; j < K_alen; ++j) acol[tc + j] = (int32_t)__ldg(la.pq + acol[tc + j]);
+        __syncwarp();
+        const uint32_t a_sa = smem_u32(aval) + (prog ? (uint32_t)tv * 8u : 0u);
+        const uint32_t c_sa = prog ? smem_u32(acol) + (uint32_t)tc * 4u : smem_u32(&T.zero);
+        const uint2 *zchunk = la.fold + la.fold_zero;
+#pragma unroll 1
+        for (int sw = 0; sw < LOCK_W; ++sw) {  // the sub-programs one after the other (each ends on a slot boundary)
+          const int c_lo = (int)((K_sub >> (8 * sw)) & 0xffu), c_hi = (int)((K_sub >> (8 * (sw + 1))) & 0xffu);
+          const int nch = c_hi - c_lo;
+          const int nchmax = __reduce_max_sync(FULL, nch);
+          const uint2 *fp = la.fold + k0.z + (size_t)c_lo * 8;
+          uint32_t o_sa = smem_u32(acc) + (uint32_t)((int)((K_s0 >> (8 * sw)) & 0xffu) * AST + lane) * 8u;
+          double a = 0.0;
+          bool fresh = true;
+#pragma unroll 1
+          for (int c = 0; c < nchmax; ++c) {
+            const uint4 *src = (const uint4 *)(c < nch ? fp + c * 8 : zchunk);
+            uint2 e[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint4 v = __ldg(src + u);
+              e[2 * u] = make_uint2(v.x, v.y);
+              e[2 * u + 1] = make_uint2(v.z, v.w);
+            }
+            double av[8], pv[8];
+            uint32_t qi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(av[u]) : "r"(a_sa + (e[u].x & 0xffu)));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qi[u]) : "r"(c_sa + (e[u].x >> 16)));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) pv[u] = __ldg(la.Q + (qi[u] + e[u].y));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const double prod = __dmul_rn(av[u], pv[u]);
+              a = fresh ? prod : __dadd_rn(a, prod);
+              fresh = false;
+              if (e[u].x & 0x8000u) {
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"(o_sa), "d"(a) : "memory");
+                o_sa += (uint32_t)AST * 8u;
+                fresh = true;
+              }
+            }
+          }
+        }
+        __syncwarp();
+      } else {
       const int nrun = T.nrun;
       const double *pbase = nrun ? pstage : op.pd_val;  // staged P rows, or global memory
       const int tc = (int)(arow - c0), tv = (int)(arow - v0);
@@ -310,6 +380,7 @@ __global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric
           }
         }
         run += ple;
+      }
       }
       __syncwarp();
       // ---- the ring slot must have been read by every reader of its previous
@@ -466,17 +537,23 @@ size_t tile_smem_layout(TileArgs &ta, int amax_blk, int pvmax, int prmax) {
   return o;
 }
 
-cudaError_t launch_tile_numeric(const Ops &op, const MapArgs &mp, const TileArgs &ta, const int64_t *c_rp,
-                                double *c_val, int blk_lo, int blk_hi, bool new_pass, cudaStream_t st) {
+cudaError_t launch_tile_numeric(const Ops &op, const MapArgs &mp, const TileArgs &ta, const LockArgs &la,
+                                const int64_t *c_rp, double *c_val, int blk_lo, int blk_hi, bool new_pass,
+                                cudaStream_t st) {
   if (new_pass) k_tile_begin<<<1, 1, 0, st>>>(ta.ctl);
   else k_tile_ticket_reset<<<1, 1, 0, st>>>(ta.ctl);
+  // the lockstep fold reads P's values class-major: refresh the copy once per pass
+  if (new_pass && la.cls != nullptr) {
+    cudaError_t pe = launch_lock_permute_f64(la.nloc, op.pd_rp, la.pq, la.ltab, op.pd_val, la.Q, st);
+    if (pe != cudaSuccess) return pe;
+  }
   // the last range of a pass also runs the gather-only items of the delay
   const int item_hi = blk_hi >= ta.nblk ? ta.nitems : blk_hi;
   if (item_hi <= blk_lo) return cudaGetLastError();
   cudaError_t e = cudaFuncSetAttribute(k_tile_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, ta.sm_total);
   if (e != cudaSuccess) return e;
   const int grid = std::min(ta.grid, item_hi - blk_lo);
-  k_tile_numeric<<<grid, NT, ta.sm_total, st>>>(op, mp, ta, c_rp, c_val, blk_lo, std::min(blk_hi, ta.nblk),
+  k_tile_numeric<<<grid, NT, ta.sm_total, st>>>(op, mp, ta, la, c_rp, c_val, blk_lo, std::min(blk_hi, ta.nblk),
                                                      item_hi);
   return cudaGetLastError();
 }
