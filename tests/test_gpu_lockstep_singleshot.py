@@ -183,3 +183,22 @@ def test_lockstep_kernel_flags_in_place_structure_edits():
     with pytest.raises(StructuralDriftError):
         plan.check()
     rp[k] -= 1
+
+
+@pytest.mark.parametrize("single", [True, False])
+def test_arena_growth_path(single, monkeypatch):
+    """An undersized first arena (PTAP_ARENA_SHRINK) overflows and is grown:
+    the single-shot pass recomputes its values into the grown arena, the
+    arena symbolic phase re-runs its pass; C matches the oracle either way."""
+    monkeypatch.setenv("PTAP_ARENA_SHRINK", "6")
+    monkeypatch.setenv("PTAP_NO_UNION", "1")  # the arena path also without single_shot
+    A, P = gen.config_operands(gen.CONFIGS["cfg3"], n_fine=12)
+    want = _oracle(A, P)
+    ctx = pk.single_rank_context()
+    a, p = pk.distribute(A, P, 1, 0)
+    c, plan = pk.ptap(a, p, "allatonce", ctx, single_shot=single)
+    assert plan.values_ready == single
+    g = pk.assemble_global([c.local], ncols=P.ncols)
+    pattern = np.array_equal(g.row_offsets, want.row_ptr) and np.array_equal(g.col_indices, want.col)
+    assert pattern
+    assert row_scaled_err(want.row_ptr, g.values, want.val) <= TOL
