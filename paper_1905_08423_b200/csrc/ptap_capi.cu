@@ -1185,7 +1185,10 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   LockClass *cls = nullptr;
   CKS(palloc(p, &cls, ncls, CAT_PLAN, st));
   l.cls = cls;
-  CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, pure, st));
+  // warps per group: long programs (27-point stencils: ~90 pairs per row) split three ways, short ones two
+  l.lw = p->nloc > 0 && (double)p->cnt.mac_ap / (double)p->nloc >= 48.0 ? 3 : 2;
+  if (const char *lwv = getenv("PTAP_LOCK_WARPS")) l.lw = atoi(lwv) == 3 ? 3 : 2;
+  CK(launch_lock_headers(ncls, op, plen8, p->maps, reps, ltab, cls, st8, st8 + 4, pure, l.lw, st));
   CKS(palloc(p, &rowinfo, n, CAT_PLAN, st));
   l.rowinfo = rowinfo;
   uint32_t *rowcls = nullptr;
@@ -1218,7 +1221,7 @@ ptap_status build_lock(ptap_plan *p, const Ops &op, const ptap_operands *ops, cu
   l.fold_zero = (uint32_t)h[1];
   CKS(palloc(p, &outer, (int64_t)h[2] + 32, CAT_PLAN, st));
   l.fold = fold; l.outer = outer;
-  CK(launch_lock_programs(ncls, op, plen8, p->maps, reps, ltab, cls, fold, outer, st));
+  CK(launch_lock_programs(ncls, op, plen8, p->maps, reps, ltab, cls, fold, outer, l.lw, st));
   drop_transient();
   // the C row starts in Q order replace the per-entry map of the q4a kernel
   int32_t *cbq = nullptr;

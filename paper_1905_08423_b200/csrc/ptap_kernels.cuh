@@ -252,19 +252,17 @@ cudaError_t launch_tile_scan32(const int32_t *in, int32_t *out, int n, void *scr
 constexpr int LOCK_TILE = 64;  // fine rows per tile
 constexpr int LOCK_NLEN = 9;   // P row lengths 0..8
 constexpr int LOCK_TABLE = 65536;  // class table slots (a plan with more than half as many classes is not eligible)
-#ifndef PTAP_LOCK_WARPS
-#define PTAP_LOCK_WARPS 3  // measured on config 3: 2 -> 4.91 ms, 3 -> 4.72, 4 -> 4.77
-#endif
-constexpr int LOCK_W = PTAP_LOCK_WARPS;  // warps per group of 32 rows (<= 7)
+constexpr int LOCK_WMAX = 4;  // most warps per group of 32 rows (the plan picks 2 or 3: LockArgs.lw)
 struct __align__(16) LockClass {  // one structural class of fine rows (32 bytes)
   uint8_t alen, nap, ntg, niter;  // A row length, AP slots, own P entries (targets), outer-program words / 32
   int32_t tstride;                // rows of P with ntg entries: stride of the row's own entries in Q
   uint32_t fold_off, outer_off;   // program offsets (entries / words)
-  uint8_t sub[8];                 // fold sub-program w = chunks [sub[w], sub[w+1]) of 8 entries (slot ranges, balanced)
+  uint8_t sub[8];                 // fold sub-program w = chunks [sub[w], sub[w+1]) of 8 entries (slot ranges, balanced); sub[7] = all chunks
   uint8_t s0[8];                  // first AP slot of sub-program w
 };
 struct LockArgs {
   int32_t nloc, ntiles, acap, aps;  // acap: staged A entries per tile, aps: AP buffer stride (doubles, odd)
+  int32_t lw;                       // warps per group of 32 rows: they split the fold by slot ranges, the outer products by rows
   uint32_t fold_zero;               // index of eight zero entries behind the fold programs
   int32_t ast;                      // odd stride (words) of the converted column rows, >= the longest A row
   int32_t dbg;                      // timing experiments only (PTAP_LOCK_DBG): 1 no outer products, 2 no fold, 4 no column conversion
@@ -293,11 +291,11 @@ cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64
                                 const uint8_t *pure, cudaStream_t st);
 cudaError_t launch_lock_headers(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                 const uint32_t *reps, const int32_t *ltab, LockClass *cls,
-                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure,
+                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure, int lw,
                                 cudaStream_t st);
 cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                  const uint32_t *reps, const int32_t *ltab, const LockClass *cls, uint2 *fold,
-                                 uint32_t *outer, cudaStream_t st);
+                                 uint32_t *outer, int lw, cudaStream_t st);
 cudaError_t launch_lock_rowinfo(int64_t n, const int64_t *ad_rp, const uint16_t *slot_of, const int32_t *slot2cls,
                                 uint32_t *rowinfo, uint32_t *rowcls, unsigned long long *amax, cudaStream_t st);
 

@@ -45,7 +45,6 @@ namespace ptapdev {
 namespace {
 
 constexpr int LT = LOCK_TILE;  // fine rows per tile
-constexpr int LW = LOCK_W;  // warps per group of 32 rows (they split the fold by slots, the outer products by rows)
 constexpr int TGS = 33;              // stride of the per-target arrays (bank-conflict free both ways)
 constexpr unsigned FULLM = 0xffffffffu;
 
@@ -103,6 +102,7 @@ __device__ __forceinline__ unsigned long long lk_mix(unsigned long long x) {
 // { ap[32 * aps], tgv[8 * TGS], tgc[8 * TGS] } | mbarrier
 // ---------------------------------------------------------------------------
 constexpr int LG = LT / 32;  // groups per tile
+template <int LW>
 __device__ __forceinline__ void lk_group_bar(int g) {
   if (g == 0)
     asm volatile("bar.sync 1, %0;" ::"n"(LW * 32) : "memory");
@@ -110,6 +110,7 @@ __device__ __forceinline__ void lk_group_bar(int g) {
     asm volatile("bar.sync 2, %0;" ::"n"(LW * 32) : "memory");
 }
 
+template <int LW>
 __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs la, double *__restrict__ c_val,
                                                                int tile0, int *status) {
   extern __shared__ __align__(16) unsigned char lsm[];
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
   const uint32_t K_tstride = k0.y, K_fold_off = k0.z, K_outer_off = k0.w;
   const unsigned long long K_sub = ((unsigned long long)k1.y << 32) | k1.x, K_s0 = ((unsigned long long)k1.w << 32) | k1.z;
   const int sub_lo = (int)((K_sub >> (8 * w)) & 0xffu), sub_hi = (int)((K_sub >> (8 * (w + 1))) & 0xffu);
-  const int sub_all = (int)((K_sub >> (8 * LW)) & 0xffu), slot0 = (int)((K_s0 >> (8 * w)) & 0xffu);
+  const int sub_all = (int)(K_sub >> 56), slot0 = (int)((K_s0 >> (8 * w)) & 0xffu);
   const uint32_t aval_sa = sm_u32(aval), acol_sa = sm_u32(acol);
   const uint32_t ap_sa0 = sm_u32(ap), tgv_sa = sm_u32(tgv), tgc_sa = sm_u32(tgc);
 
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
       tgc[jt * TGS + lane] = __ldg(la.cbQ + x);
     }
   }
-  lk_group_bar(g);
+  lk_group_bar<LW>(g);
 
   // fold, slot-major: warp w folds the slots of its range of the lane's class
   // program; one register accumulator, stored once per slot.  Entries past a
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(LG * LW * 32) k_lock_numeric(Ops op, LockArgs 
       }
     }
   }
-  lk_group_bar(g);
+  lk_group_bar<LW>(g);
 
   // outer products, transposed: the lanes take the (target, slot) items of
   // row r's class; warp w takes rows w, w + LW, ...  The decoded program words
@@ -358,13 +359,18 @@ cudaError_t launch_lock_numeric(const Ops &op, const LockArgs &la, double *c_val
                                 int *status, cudaStream_t st) {
   if (tile_hi <= tile_lo) return cudaSuccess;
   const size_t sm = lock_smem_bytes(la);
-  static size_t opted = 0;
-  if (sm > opted) {
-    cudaError_t e = cudaFuncSetAttribute(k_lock_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  static size_t opted[LOCK_WMAX + 1] = {0};
+  const int lw = la.lw == 3 ? 3 : 2;
+  if (sm > opted[lw]) {
+    cudaError_t e = lw == 3 ? cudaFuncSetAttribute(k_lock_numeric<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)
+                            : cudaFuncSetAttribute(k_lock_numeric<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    opted = sm;
+    opted[lw] = sm;
   }
-  k_lock_numeric<<<tile_hi - tile_lo, LG * LW * 32, sm, st>>>(op, la, c_val, tile_lo, status);
+  if (lw == 3)
+    k_lock_numeric<3><<<tile_hi - tile_lo, LG * 3 * 32, sm, st>>>(op, la, c_val, tile_lo, status);
+  else
+    k_lock_numeric<2><<<tile_hi - tile_lo, LG * 2 * 32, sm, st>>>(op, la, c_val, tile_lo, status);
   return cudaGetLastError();
 }
 
@@ -585,9 +591,9 @@ __global__ void __launch_bounds__(1024) k_lock_compact(int tbl, const unsigned l
 }
 
 // pairs per AP slot of the class represented by row r, and the cut of the
-// slots into LOCK_W contiguous ranges of about equal pair counts
+// slots into lw contiguous ranges of about equal pair counts
 __device__ void lock_class_split(const Ops &op, const uint8_t *plen8, const uint8_t *sm, int64_t a0, int alen, int nap,
-                                 int *cnt, int *first, int *pairs) {
+                                 int lw, int *cnt, int *first, int *pairs) {
   for (int s = 0; s < 32; ++s) cnt[s] = 0;
   int p = 0;
   for (int j = 0; j < alen; ++j) {
@@ -596,25 +602,25 @@ __device__ void lock_class_split(const Ops &op, const uint8_t *plen8, const uint
   }
   const int np = p;
   int s = 0, cum = 0;
-  for (int w = 0; w < LOCK_W; ++w) {
+  for (int w = 0; w < lw; ++w) {
     first[w] = s;
     int mine = 0;
-    const int want = (int)(((long long)np * (w + 1)) / LOCK_W);
-    while (s < nap && (w == LOCK_W - 1 || cum + cnt[s] <= want || mine == 0)) {
+    const int want = (int)(((long long)np * (w + 1)) / lw);
+    while (s < nap && (w == lw - 1 || cum + cnt[s] <= want || mine == 0)) {
       mine += cnt[s];
       cum += cnt[s];
       ++s;
     }
     pairs[w] = mine;
   }
-  first[LOCK_W] = nap;
+  first[lw] = nap;
 }
 
 // class headers and program offsets (one CTA): out[1] fold entries, out[2] outer words
 __global__ void __launch_bounds__(1024) k_lock_headers(int ncls, Ops op, const uint8_t *plen8, const int64_t *smap_rp,
                                                        const uint8_t *smap, const uint8_t *nap, const uint32_t *reps,
                                                        const int32_t *ltab, LockClass *cls, unsigned long long *out,
-                                                       unsigned long long *bad, const uint8_t *pure) {
+                                                       unsigned long long *bad, const uint8_t *pure, int lw) {
   typedef cub::BlockScan<unsigned, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned carry_f, carry_o;
@@ -639,16 +645,16 @@ __global__ void __launch_bounds__(1024) k_lock_headers(int ncls, Ops op, const u
         K.ntg = (uint8_t)ntg;
         K.tstride = ltab[ntg];
         if (ntg > 0 && napr > 0 && np > 0) {  // a row without targets contributes nothing
-          int cnt[32], first[LOCK_W + 1], pairs[LOCK_W];
+          int cnt[32], first[LOCK_WMAX + 1], pairs[LOCK_WMAX];
           const uint8_t *sm = smap + ((unsigned long long)__ldg(smap_rp + r) & SMAP_OFF_MASK);
-          lock_class_split(op, plen8, sm, a0, alen, napr, cnt, first, pairs);
+          lock_class_split(op, plen8, sm, a0, alen, napr, lw, cnt, first, pairs);
           int ch = 0;
-          for (int w = 0; w < LOCK_W; ++w) {
+          for (int w = 0; w < lw; ++w) {
             K.sub[w] = (uint8_t)ch;
             K.s0[w] = (uint8_t)first[w];
             ch += (pairs[w] + 7) / 8;
           }
-          for (int w = LOCK_W; w < 8; ++w) K.sub[w] = (uint8_t)ch;
+          for (int w = lw; w < 8; ++w) K.sub[w] = (uint8_t)ch;
           if (ch > 255) atomicAdd(bad, 1ull);
           fsz = (unsigned)ch * 8u;
           const int items = ntg * napr;
@@ -686,19 +692,19 @@ __global__ void __launch_bounds__(1024) k_lock_headers(int ncls, Ops op, const u
 __global__ void __launch_bounds__(128) k_lock_programs(int ncls, Ops op, const uint8_t *plen8, const int64_t *smap_rp,
                                                        const uint8_t *smap, const int64_t *pmap_rp,
                                                        const uint8_t *pmap, const uint32_t *reps, const int32_t *ltab,
-                                                       const LockClass *cls, uint2 *fold, uint32_t *outer) {
+                                                       const LockClass *cls, uint2 *fold, uint32_t *outer, int lw) {
   const int c = blockIdx.x * 128 + threadIdx.x;
   if (c >= ncls) return;
   const LockClass K = cls[c];
-  if (K.sub[LOCK_W] == 0) return;
+  if (K.sub[7] == 0) return;
   const int64_t r = reps[c];
   const int64_t a0 = __ldg(op.ad_rp + r);
   const uint8_t *sm = smap + ((unsigned long long)__ldg(smap_rp + r) & SMAP_OFF_MASK);
   uint2 *fp = fold + K.fold_off;
-  int cnt[32], pos[32], first[LOCK_W + 1], pairs[LOCK_W];
-  lock_class_split(op, plen8, sm, a0, K.alen, K.nap, cnt, first, pairs);
-  for (int q = 0; q < (int)K.sub[LOCK_W] * 8; ++q) fp[q] = make_uint2(0u, 0u);
-  for (int w = 0; w < LOCK_W; ++w) {
+  int cnt[32], pos[32], first[LOCK_WMAX + 1], pairs[LOCK_WMAX];
+  lock_class_split(op, plen8, sm, a0, K.alen, K.nap, lw, cnt, first, pairs);
+  for (int q = 0; q < (int)K.sub[7] * 8; ++q) fp[q] = make_uint2(0u, 0u);
+  for (int w = 0; w < lw; ++w) {
     int run = (int)K.sub[w] * 8;
     for (int s = first[w]; s < first[w + 1]; ++s) {
       pos[s] = run;
@@ -772,18 +778,19 @@ cudaError_t launch_lock_classes(const Ops &op, const uint8_t *plen8, const int64
 
 cudaError_t launch_lock_headers(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                 const uint32_t *reps, const int32_t *ltab, LockClass *cls,
-                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure,
+                                unsigned long long *out, unsigned long long *bad, const uint8_t *pure, int lw,
                                 cudaStream_t st) {
-  k_lock_headers<<<1, 1024, 0, st>>>(ncls, op, plen8, mp.smap_rp, mp.smap, mp.nap, reps, ltab, cls, out, bad, pure);
+  k_lock_headers<<<1, 1024, 0, st>>>(ncls, op, plen8, mp.smap_rp, mp.smap, mp.nap, reps, ltab, cls, out, bad, pure,
+                                     lw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lock_programs(int ncls, const Ops &op, const uint8_t *plen8, const MapArgs &mp,
                                  const uint32_t *reps, const int32_t *ltab, const LockClass *cls, uint2 *fold,
-                                 uint32_t *outer, cudaStream_t st) {
+                                 uint32_t *outer, int lw, cudaStream_t st) {
   if (ncls == 0) return cudaSuccess;
   k_lock_programs<<<(ncls + 127) / 128, 128, 0, st>>>(ncls, op, plen8, mp.smap_rp, mp.smap, mp.pmap_rp, mp.pmap, reps,
-                                                      ltab, cls, fold, outer);
+                                                      ltab, cls, fold, outer, lw);
   return cudaGetLastError();
 }
 

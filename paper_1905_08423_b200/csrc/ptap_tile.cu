@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric
         const int K_alen = (int)(k0.x & 0xffu);
         const unsigned long long K_sub = ((unsigned long long)k1.y << 32) | k1.x;
         const unsigned long long K_s0 = ((unsigned long long)k1.w << 32) | k1.z;
-        const bool prog = (int)((K_sub >> (8 * LOCK_W)) & 0xffu) > 0;
+        const bool prog = (int)(K_sub >> 56) > 0;
         const int tc = (int)(arow - c0), tv = (int)(arow - v0);
         if (prog)
 #pragma unroll 4
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(NT, 12 / (TW + GW) > 4 ? 5 : 4) k_tile_numeric
         const uint32_t c_sa = prog ? smem_u32(acol) + (uint32_t)tc * 4u : smem_u32(&T.zero);
         const uint2 *zchunk = la.fold + la.fold_zero;
 #pragma unroll 1
-        for (int sw = 0; sw < LOCK_W; ++sw) {  // the sub-programs one after the other (each ends on a slot boundary)
+        for (int sw = 0; sw < la.lw; ++sw) {  // the sub-programs one after the other (each ends on a slot boundary)
           const int c_lo = (int)((K_sub >> (8 * sw)) & 0xffu), c_hi = (int)((K_sub >> (8 * (sw + 1))) & 0xffu);
           const int nch = c_hi - c_lo;
           const int nchmax = __reduce_max_sync(FULL, nch);

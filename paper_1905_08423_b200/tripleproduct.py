@@ -516,8 +516,10 @@ def _numeric_streamed(a: DistMatrix, p: DistMatrix, plan: TripleProductPlan, ctx
     n = a.local.nrows
     a_rp = a.local.diag.row_offsets
     # block-aligned bounds (the plan's numeric kernels fold 64-row blocks)
-    bounds = [min(n, -(-(n * k // nblk) // 64) * 64) for k in range(nblk + 1)]
-    bounds[-1] = n
+    bounds = sorted({min(n, -(-(n * k // nblk) // 64) * 64) for k in range(nblk)} | {0, n})
+    if len(bounds) < 2:
+        bounds = [0, n]
+    nblk = len(bounds) - 1  # small operands: fewer, non-empty blocks (every bound is a multiple of 64, or n)
     a_host = torch.from_numpy(a.local.diag.values)
     p_host = torch.from_numpy(p.local.diag.values)
     a_dev, p_dev = plan._a_dev.diag.val, plan._p_dev.diag.val
