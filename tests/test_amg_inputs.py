@@ -146,3 +146,29 @@ def test_greedy_aggregation_compiled_matches_reference_loops():
     b = amg._greedy_aggregate(W.indptr, W.indices, 4000)
     assert np.array_equal(a, b)
     assert a.min() == 0 and np.all(np.diff(np.unique(a)) == 1)
+
+
+def test_parallel_greedy_aggregation_matches_sequential_loops():
+    """devgen's rounds-of-neighbourhood-minima aggregation (the device
+    generator of config 5, run here on CPU tensors) gives exactly the
+    aggregates of the sequential two-pass loops."""
+    import scipy.sparse as sp
+    import torch
+    from scipy.spatial import cKDTree
+
+    from paper_1905_08423_b200 import problems_amg as amg
+    from paper_1905_08423_b200.devgen import _greedy_aggregate_device
+
+    for npts, k, seed in ((500, 26, 1), (4000, 26, 20190520), (3000, 6, 7)):
+        pts = np.random.default_rng(seed).random((npts, 3))
+        _, nbr = cKDTree(pts).query(pts, k=k + 1)
+        indptr = np.arange(0, npts * k + 1, k, dtype=np.int64)
+        wd = sp.csr_matrix((np.ones(npts * k), nbr[:, 1:].ravel().astype(np.int64), indptr), shape=(npts, npts))
+        w = wd.maximum(wd.T.tocsr()).tocsr()
+        w.sort_indices()
+        want = amg._greedy_aggregate(w.indptr, w.indices, npts)
+        rows = torch.from_numpy(np.repeat(np.arange(npts), np.diff(w.indptr)))
+        cols = torch.from_numpy(w.indices.astype(np.int64))
+        agg, nagg = _greedy_aggregate_device(rows, cols, npts)
+        assert nagg == int(want.max()) + 1
+        assert np.array_equal(agg.numpy(), want)
